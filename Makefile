@@ -1,0 +1,38 @@
+# Build everything in-tree (the .so files travel to the GPU box with gpurun).
+#   make            -> paper_1305_3345_b200/libkgpu.so, oracle/libkgo.so, build/test_kat, build/pipes
+NVCC    ?= nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Xptxas -v
+PKG     := paper_1305_3345_b200
+CSRC    := $(PKG)/csrc
+LIB     := $(PKG)/libkgpu.so
+
+all: $(LIB) oracle/libkgo.so build/test_kat build/pipes
+
+build:
+	mkdir -p build
+
+build/%.o: $(CSRC)/%.cu $(CSRC)/kg_internal.h include/kg.h | build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
+
+build/%.o: $(CSRC)/%.cpp $(CSRC)/kg_internal.h include/kg.h | build
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
+
+$(LIB): build/kg_kernels.o build/kg_tables.o build/kg_runtime.o
+	$(NVCC) $(ARCH) -shared -cudart static -o $@.tmp $^ -Xcompiler -fvisibility=hidden && mv $@.tmp $@
+
+# ORACLE (test infrastructure; never linked into the product)
+oracle/libkgo.so: oracle/kgo_aes.c oracle/kgo_pages.c oracle/kgo_aes.h
+	gcc -std=c99 -O2 -fPIC -shared -D_POSIX_C_SOURCE=200809L -Wall -o $@ oracle/kgo_aes.c oracle/kgo_pages.c -lpthread
+
+build/test_kat: oracle/kgo_aes.c oracle/kgo_pages.c oracle/test_kat.c oracle/kgo_aes.h | build
+	gcc -std=c99 -O2 -D_POSIX_C_SOURCE=200809L -Wall -o $@ oracle/kgo_aes.c oracle/kgo_pages.c oracle/test_kat.c -lpthread
+
+# pipe microbenchmarks (roofline inputs)
+build/pipes: tools/pipes.cu | build
+	$(NVCC) -O3 -lineinfo -std=c++17 $(ARCH) -o $@ $<
+
+clean:
+	rm -rf build $(LIB) oracle/libkgo.so
+
+.PHONY: all clean

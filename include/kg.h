@@ -1,0 +1,155 @@
+/*
+ * kg.h -- C ABI of the B200-native KGPU page-crypto library (libkgpu.so).
+ *
+ * The one hot path of KGPU (arXiv 1305.3345) that this library implements:
+ * AES encryption/decryption of batches of independent fixed-size pages,
+ * offloaded from the OS to the GPU "as a service ... for the Linux crypto
+ * subsystem" (§3.3), for "kernel tasks that depend on
+ * per-page encryption/decryption, such as encrypted filesystems"
+ * (PAPER.md:464-466).  Mode: CBC with one chain per page and a per-page IV
+ * (BASELINE.json:5; the paper's own ECB, is KG_MODE_ECB).
+ *
+ * The call protocol follows the paper's four steps (§3.2):
+ *   "requests one of the pinned-memory buffers, and fills it"  -> caller owns
+ *        device or pinned-host buffers ("pinned memory
+ *        for all buffers");
+ *   "builds a service request"                                  -> arguments
+ *        of kg_submit_pages (service = dir/mode, input/output buffers);
+ *   "places the service request into request queue"             -> kg_submit_pages
+ *        returns a ticket once the work is enqueued;
+ *   "waits ... either by blocking ... or busy-waiting on the response
+ *        queue"                                                  -> kg_wait / kg_poll.
+ *
+ * Conventions
+ *   - Status: 0 = KG_OK, negative = error (KG_E*).  No exceptions, no
+ *     longjmp, no torch types cross this boundary.
+ *   - One context per process, bound to one GPU by kg_init (multi-GPU =
+ *     one process per GPU).  Every call is thread-safe.
+ *   - Any call other than kg_strerror/kg_launch_count before kg_init
+ *     returns KG_ENOTINIT.
+ *   - Argument errors are detected synchronously, before anything is
+ *     enqueued; nothing is written to any caller buffer.
+ *
+ * Layout of a batch (all byte offsets are 64-bit):
+ *   in / out : [n_pages][page_bytes] uint8, contiguous, 16-byte aligned.
+ *              Page p, block j (16 bytes) lives at byte p*page_bytes + 16*j.
+ *   ivs      : [n_pages][16] uint8, 16-byte aligned; page p's IV at 16*p,
+ *              used raw as C_{p,-1} (SP 800-38A §6.2).  Ignored (may be NULL)
+ *              for KG_MODE_ECB.
+ *
+ * Memory kinds: each of in, out, ivs must be device memory of the context's
+ * GPU (or managed memory) or page-locked ("pinned") host memory registered
+ * with CUDA.  Pageable host memory -> KG_EINVAL.  Mixed kinds are allowed.
+ * Device batches run on `stream`; batches touching host memory are staged
+ * through the library's device staging ring (3 slots by default, after
+ * PAPER.md:437-440) on internal copy/compute streams overlapped with each
+ * other, joined back onto `stream`.
+ */
+#ifndef KG_H
+#define KG_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KG_API __attribute__((visibility("default")))
+#else
+#define KG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Cipher direction (PAPER.md:445-447 encryption; 470-471 decryption). */
+#define KG_ENCRYPT 0
+#define KG_DECRYPT 1
+
+/* Chaining mode.  CBC = NIST SP 800-38A §6.2, one chain per page
+ * (BASELINE.json:5).  ECB = SP 800-38A §6.1, the paper's mode "for maximum
+ * parallelism". */
+#define KG_MODE_CBC 0
+#define KG_MODE_ECB 1
+
+/* Status codes. */
+#define KG_OK        0
+#define KG_EINVAL   -1  /* bad argument (see kg_submit_pages)                 */
+#define KG_ENOKEY   -2  /* key_id has no key set                              */
+#define KG_ENOTINIT -3  /* kg_init not called (or after kg_shutdown)          */
+#define KG_EAGAIN   -4  /* ticket table full: wait on an older ticket first   */
+#define KG_ENOMEM   -5  /* device staging allocation failed                   */
+#define KG_ECUDA    -6  /* CUDA runtime/driver error (sticky: kg_shutdown +   */
+                        /* kg_init to recover)                                */
+#define KG_ENOTSUP  -7  /* unsupported (e.g. no sm_100 device)                */
+#define KG_ETICKET  -8  /* unknown, retired or already-claimed ticket         */
+
+#define KG_MAX_KEYS 256
+#define KG_MAX_INFLIGHT 65536
+
+/* Bind this process to GPU `device`, build the device lookup tables, create
+ * the internal streams.  Idempotent for the same device; a different device
+ * while initialised -> KG_EINVAL.  Errors: KG_EINVAL (no such device),
+ * KG_ENOTSUP (device is not compute capability 10.x), KG_ECUDA. */
+KG_API int kg_init(int device);
+
+/* Expand `key` (16, 24 or 32 bytes: AES-128/192/256, FIPS-197 §5.2
+ * KeyExpansion) into encryption and equivalent-inverse-cipher decryption
+ * round keys (FIPS-197 §5.3.5) and store them under key_id.  The key bytes
+ * are copied; the caller may wipe its buffer on return.  Re-keying a key_id
+ * never affects batches already submitted (keys are snapshotted at submit).
+ * Errors: KG_ENOTINIT; KG_EINVAL (key NULL, key_bytes not 16/24/32, key_id
+ * outside [0, KG_MAX_KEYS)). */
+KG_API int kg_set_key(int key_id, const uint8_t *key, int key_bytes);
+
+/* Submit one batch: `dir` (KG_ENCRYPT/KG_DECRYPT) in `mode` (KG_MODE_CBC/
+ * KG_MODE_ECB) of n_pages pages of page_bytes each from `in` to `out`
+ * (out == in, an exact alias, is allowed and gives the same bytes as
+ * out-of-place), with page p's IV at ivs + 16p, under key `key_id`, ordered
+ * after all work already enqueued on `stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  Work enqueued on `stream` after this call sees
+ * the outputs.
+ * Returns a ticket >= 0 (strictly increasing per process) or a status < 0:
+ *   KG_EINVAL: dir/mode out of range; n_pages == 0; page_bytes == 0 or not a
+ *     multiple of 16 (no padding); n_pages*page_bytes overflows 64 bits; a
+ *     required pointer NULL or not 16-byte aligned; in/out partially
+ *     overlapping; ivs overlapping out; key_id out of range; a pointer that
+ *     is pageable host memory or another GPU's memory.
+ *   KG_ENOKEY, KG_ENOTINIT, KG_EAGAIN, KG_ENOMEM, KG_ECUDA (launch failure).
+ * Ownership: the caller owns in/out/ivs and keeps them valid and unmodified
+ * until kg_wait/kg_poll reports completion; the library retains nothing
+ * after completion. */
+KG_API int64_t kg_submit_pages(int dir, int mode, const void *in, void *out,
+                        uint64_t n_pages, uint32_t page_bytes,
+                        const void *ivs, int key_id, void *stream);
+
+/* Block until the batch of `ticket` has completed; retire the ticket.
+ * Returns KG_OK, KG_ECUDA (an asynchronous device fault), KG_ETICKET
+ * (unknown / already retired / being waited on by another thread). */
+KG_API int kg_wait(int64_t ticket);
+
+/* Non-blocking completion check (the paper's busy-wait mode).
+ * Returns 1 = done, 0 = pending, < 0 = error (KG_ETICKET, KG_ECUDA).  Does not
+ * retire the ticket: call kg_wait (which then returns at once) to retire. */
+KG_API int kg_poll(int64_t ticket);
+
+/* Drain all outstanding work, free the staging ring, streams, events and
+ * tables, forget all keys.  KG_ENOTINIT if not initialised. */
+KG_API int kg_shutdown(void);
+
+/* Static description of a status code; never NULL. */
+KG_API const char *kg_strerror(int status);
+
+/* Staging pipeline for batches touching host memory: chunk size in bytes
+ * (rounded down to whole pages, at least one page) and number of device
+ * staging slots (2..8).  Takes effect for later submits.  Defaults: 8 MiB,
+ * 3 slots ("three buffers").  Environment overrides at
+ * kg_init: KG_CHUNK_BYTES, KG_STAGING_SLOTS.  KG_EINVAL on bad values. */
+KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);
+
+/* Number of CUDA kernels this library has launched in this process
+ * (instrumentation for benchmarks; monotonic, never reset). */
+KG_API uint64_t kg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KG_H */

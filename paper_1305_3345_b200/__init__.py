@@ -1,0 +1,152 @@
+"""Thin Python binding of the KGPU page-crypto C ABI (include/kg.h).
+
+Argument marshalling only: every step of the hot path runs in
+libkgpu.so's CUDA kernels and runtime.  The names mirror the C ABI without
+the ``kg_`` prefix.  torch is used only to hand in tensors (device or pinned
+host memory) and streams; any other object exposing ``data_ptr()`` or a
+raw integer address also works.
+
+There is no CPU fallback: if libkgpu.so is missing, importing this module
+raises ImportError (build it with ``make`` or ``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkgpu.so")
+
+ENCRYPT, DECRYPT = 0, 1
+MODE_CBC, MODE_ECB = 0, 1
+OK, EINVAL, ENOKEY, ENOTINIT, EAGAIN, ENOMEM, ECUDA, ENOTSUP, ETICKET = 0, -1, -2, -3, -4, -5, -6, -7, -8
+MAX_KEYS = 256
+MAX_INFLIGHT = 65536
+
+#: every symbol include/kg.h declares
+ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
+               "kg_strerror", "kg_set_pipeline", "kg_launch_count")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `make` (or __graft_entry__.build()); "
+                      "there is no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_lib.kg_init.argtypes = [ctypes.c_int]
+_lib.kg_init.restype = ctypes.c_int
+_lib.kg_set_key.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
+_lib.kg_set_key.restype = ctypes.c_int
+_lib.kg_submit_pages.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                 ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+_lib.kg_submit_pages.restype = ctypes.c_int64
+_lib.kg_wait.argtypes = [ctypes.c_int64]
+_lib.kg_wait.restype = ctypes.c_int
+_lib.kg_poll.argtypes = [ctypes.c_int64]
+_lib.kg_poll.restype = ctypes.c_int
+_lib.kg_shutdown.argtypes = []
+_lib.kg_shutdown.restype = ctypes.c_int
+_lib.kg_strerror.argtypes = [ctypes.c_int]
+_lib.kg_strerror.restype = ctypes.c_char_p
+_lib.kg_set_pipeline.argtypes = [ctypes.c_uint64, ctypes.c_int]
+_lib.kg_set_pipeline.restype = ctypes.c_int
+_lib.kg_launch_count.argtypes = []
+_lib.kg_launch_count.restype = ctypes.c_uint64
+
+
+class KgError(RuntimeError):
+    def __init__(self, code: int, where: str = ""):
+        self.code = int(code)
+        super().__init__(f"{where}: {strerror(code)} ({code})" if where else f"{strerror(code)} ({code})")
+
+
+def _check(rc: int, where: str) -> int:
+    if rc < 0:
+        raise KgError(rc, where)
+    return rc
+
+
+def _addr(x) -> int | None:
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):  # numpy (must be pinned/registered to be accepted)
+        return x.ctypes.data
+    raise TypeError(f"cannot take the address of {type(x)!r}")
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    if hasattr(s, "cuda_stream"):
+        return s.cuda_stream
+    raise TypeError(f"not a stream: {type(s)!r}")
+
+
+def strerror(code: int) -> str:
+    return _lib.kg_strerror(int(code)).decode()
+
+
+def init(device: int = 0) -> None:
+    _check(_lib.kg_init(int(device)), "kg_init")
+
+
+def set_key(key_id: int, key: bytes) -> None:
+    key = bytes(key)
+    _check(_lib.kg_set_key(int(key_id), key, len(key)), "kg_set_key")
+
+
+def submit_pages(direction: int, mode: int, inp, out, n_pages: int, page_bytes: int, ivs, key_id: int,
+                 stream=None) -> int:
+    """Enqueue one batch; returns the ticket (raises KgError on a negative status)."""
+    rc = _lib.kg_submit_pages(int(direction), int(mode), _addr(inp), _addr(out), int(n_pages), int(page_bytes),
+                              _addr(ivs), int(key_id), _stream(stream))
+    return _check(rc, "kg_submit_pages")
+
+
+def submit_pages_raw(direction, mode, inp, out, n_pages, page_bytes, ivs, key_id, stream=None) -> int:
+    """Like submit_pages but returns the raw status/ticket without raising."""
+    return _lib.kg_submit_pages(int(direction), int(mode), _addr(inp), _addr(out), int(n_pages), int(page_bytes),
+                                _addr(ivs), int(key_id), _stream(stream))
+
+
+def wait(ticket: int) -> None:
+    _check(_lib.kg_wait(int(ticket)), "kg_wait")
+
+
+def wait_raw(ticket: int) -> int:
+    return _lib.kg_wait(int(ticket))
+
+
+def poll(ticket: int) -> bool:
+    return bool(_check(_lib.kg_poll(int(ticket)), "kg_poll"))
+
+
+def poll_raw(ticket: int) -> int:
+    return _lib.kg_poll(int(ticket))
+
+
+def shutdown() -> None:
+    _check(_lib.kg_shutdown(), "kg_shutdown")
+
+
+def set_pipeline(chunk_bytes: int, slots: int) -> None:
+    _check(_lib.kg_set_pipeline(int(chunk_bytes), int(slots)), "kg_set_pipeline")
+
+
+def launch_count() -> int:
+    return int(_lib.kg_launch_count())
+
+
+def crypt_pages(direction: int, mode: int, inp, out, n_pages: int, page_bytes: int, ivs, key_id: int,
+                stream=None) -> None:
+    """submit_pages + wait."""
+    wait(submit_pages(direction, mode, inp, out, n_pages, page_bytes, ivs, key_id, stream))
+
+
+def raw_lib():
+    return _lib

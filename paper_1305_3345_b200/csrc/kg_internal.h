@@ -1,0 +1,51 @@
+// kg_internal.h -- shared between the runtime (kg_runtime.cpp) and the
+// kernels (kg_kernels.cu).  Product code only; nothing here is shared with
+// oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kg {
+
+// Round keys as little-endian 32-bit column words: byte r of word c is
+// state row r of column c (FIPS-197 §3.4 state s[r][c] = in[r + 4c]).
+// Encryption: rk[4r + c] = w[4r + c] (FIPS-197 §5.2).
+// Decryption: the equivalent inverse cipher's schedule in order of use
+// (FIPS-197 §5.3.5): rk[0..3] = w[Nr], rk[4r..] = InvMixColumns(w[Nr-r])
+// for 0 < r < Nr, rk[4Nr..] = w[0].
+struct RoundKeys {
+    uint32_t w[60];
+};
+
+// Everything one kernel launch needs, passed BY VALUE as the kernel
+// parameter (the key words are then constant-bank operands that ptxas folds
+// straight into LOP3 XORs).
+struct LaunchArgs {
+    const uint4 *in;      // [n_pages * m] 16-byte blocks
+    uint4 *out;           // same layout; may equal in
+    const uint4 *ivs;     // [n_pages] (CBC only)
+    uint64_t n_pages;
+    uint32_t m;           // blocks per page = page_bytes / 16
+    uint32_t in_place;    // out == in
+    RoundKeys rk;
+};
+
+// Base (unreplicated) lookup tables, built on the host by the GPU-path code
+// (kg_tables.cpp) and copied to the device once at kg_init.
+struct BaseTables {
+    uint32_t te0[256];    // Te0[x] = {02}S(x) | S(x)<<8 | S(x)<<16 | {03}S(x)<<24
+    uint32_t td0[256];    // Td0[x] = {0e}Si(x) | {09}Si(x)<<8 | {0d}Si(x)<<16 | {0b}Si(x)<<24
+    uint32_t isb4[256];   // Si(x) * 0x01010101
+};
+
+// kg_tables.cpp
+void build_base_tables(BaseTables *t);
+int expand_key(const uint8_t *key, int key_bytes, RoundKeys *enc, RoundKeys *dec);  // returns Nr or -1
+
+// kg_kernels.cu
+cudaError_t kernels_init(const BaseTables &t);
+// Enqueue one batch on `st`.  dir/mode/nr validated by the caller.
+cudaError_t launch_pages(int dir, int mode, int nr, const LaunchArgs &a, int num_sms, cudaStream_t st);
+
+}  // namespace kg

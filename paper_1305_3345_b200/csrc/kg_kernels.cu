@@ -1,0 +1,309 @@
+// kg_kernels.cu -- the AES page kernels for sm_100a.
+//
+// What they compute (exactly, bit for bit): FIPS-197 AES over 16-byte
+// blocks, chained per page as NIST SP 800-38A §6.2 CBC (one chain per page,
+// per-page IV, BASELINE.json:5) or §6.1 ECB (the paper's mode).
+// Decryption uses the equivalent inverse cipher (FIPS-197 §5.3.5) with the
+// schedule kg_tables.cpp prepares.
+//
+// B200 design:
+//  * The bound is the shared-memory data path (32 lane-lookups/clk/SM), not
+//    HBM and not tensor cores: 16 table lookups per block-round.
+//  * T-tables live in shared memory replicated 32x so that lane l only ever
+//    touches bank l (conflict-free by construction).  Entry x of table i
+//    for lane l sits at byte  (i>>1)*64K + x*256 + (i&1)*128 + l*4.  One
+//    PRMT (__byte_perm) turns (state word, lane bytes) into that offset, so a
+//    lookup is exactly PRMT + LDS; the region base is an LDS immediate.
+//  * Round keys come by value in the kernel parameter (constant bank), so
+//    AddRoundKey folds into the 3-input LOP3 XOR trees for free.
+//  * Block-parallel kernel (CBC decrypt, ECB both ways): each warp streams a
+//    contiguous range of 16-byte blocks, one block per lane, 512-byte
+//    coalesced LDG.128/STG.128 per warp; the CBC predecessor C_{j-1} comes
+//    from the neighbouring lane by SHFL (lane 0: the previous unit's lane 31,
+//    or the IV at a page start).
+//  * Chain kernel (CBC encrypt, serial within a page): one thread per page
+//    chain, pages balanced over a persistent grid of one CTA per SM.
+//  * In-place safety (out == in): CTAs own whole pages; inside a CTA every
+//    warp snapshots the one predecessor block it needs from another warp
+//    BEFORE the CTA-wide barrier that precedes the first store.
+#include <stdint.h>
+
+#include "kg_internal.h"
+
+namespace kg {
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kRegion = 65536;
+constexpr int kSmemEnc = 2 * kRegion;                       // Te0..Te3
+constexpr int kSmemDec = 2 * kRegion + 255 * 256 + 128;     // Td0..Td3 + Si (t = 0 slots only)
+
+__device__ BaseTables g_tables;
+
+__device__ __forceinline__ uint32_t rotl32(uint32_t v, int s) { return __funnelshift_l(v, v, s); }
+
+// Replicate the 256-entry base tables into the lane-private layout.
+template <bool DEC>
+__device__ __forceinline__ void fill_tables(char *sm) {
+    for (int idx = threadIdx.x; idx < 256 * 32; idx += blockDim.x) {
+        const int x = idx >> 5, l = idx & 31;
+        const uint32_t v = DEC ? g_tables.td0[x] : g_tables.te0[x];
+        const int o = x * 256 + l * 4;
+        *reinterpret_cast<uint32_t *>(sm + o) = v;
+        *reinterpret_cast<uint32_t *>(sm + o + 128) = rotl32(v, 8);
+        *reinterpret_cast<uint32_t *>(sm + kRegion + o) = rotl32(v, 16);
+        *reinterpret_cast<uint32_t *>(sm + kRegion + o + 128) = rotl32(v, 24);
+        if (DEC) *reinterpret_cast<uint32_t *>(sm + 2 * kRegion + o) = g_tables.isb4[x];
+    }
+}
+
+// Table I (0..3) looked up with byte I of x:  T_I[x.byte(I)].
+template <int I>
+__device__ __forceinline__ uint32_t T(const char *sm, uint32_t x, uint32_t lb) {
+    constexpr uint32_t sel = 0x7700u | (I << 4) | (4 + (I & 1));
+    const uint32_t off = __byte_perm(x, lb, sel);
+    return *reinterpret_cast<const uint32_t *>(sm + (I >> 1) * kRegion + off);
+}
+
+// Inverse S-box (replicated in all four bytes) looked up with byte K of x.
+template <int K>
+__device__ __forceinline__ uint32_t IS(const char *sm, uint32_t x, uint32_t lb) {
+    constexpr uint32_t sel = 0x7700u | (K << 4) | 4;
+    const uint32_t off = __byte_perm(x, lb, sel);
+    return *reinterpret_cast<const uint32_t *>(sm + 2 * kRegion + off);
+}
+
+// ---- encryption: FIPS-197 §5.1 rounds in T-table form ----------------------
+// Input s already XORed with round key 0 (and, for CBC, with C_{j-1}).
+template <int NR>
+__device__ __forceinline__ uint4 encrypt_rounds(const char *sm, uint32_t lb, uint4 s, const RoundKeys &rk) {
+    uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+        const uint32_t t0 = T<0>(sm, s0, lb) ^ T<1>(sm, s1, lb) ^ T<2>(sm, s2, lb) ^ T<3>(sm, s3, lb) ^ rk.w[4 * r + 0];
+        const uint32_t t1 = T<0>(sm, s1, lb) ^ T<1>(sm, s2, lb) ^ T<2>(sm, s3, lb) ^ T<3>(sm, s0, lb) ^ rk.w[4 * r + 1];
+        const uint32_t t2 = T<0>(sm, s2, lb) ^ T<1>(sm, s3, lb) ^ T<2>(sm, s0, lb) ^ T<3>(sm, s1, lb) ^ rk.w[4 * r + 2];
+        const uint32_t t3 = T<0>(sm, s3, lb) ^ T<1>(sm, s0, lb) ^ T<2>(sm, s1, lb) ^ T<3>(sm, s2, lb) ^ rk.w[4 * r + 3];
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    // Final round (no MixColumns): S(x) is byte (I+1)%4 of T_I[x]; gather the
+    // four S bytes of each column with PRMT, then AddRoundKey.
+    uint4 o;
+#define KG_ENC_LAST(dst, a, b, c, d, kw)                                                                  \
+    dst = __byte_perm(__byte_perm(T<0>(sm, a, lb), T<1>(sm, b, lb), 0x0061u),                             \
+                      __byte_perm(T<2>(sm, c, lb), T<3>(sm, d, lb), 0x4300u), 0x7610u) ^ rk.w[4 * NR + kw];
+    KG_ENC_LAST(o.x, s0, s1, s2, s3, 0)
+    KG_ENC_LAST(o.y, s1, s2, s3, s0, 1)
+    KG_ENC_LAST(o.z, s2, s3, s0, s1, 2)
+    KG_ENC_LAST(o.w, s3, s0, s1, s2, 3)
+#undef KG_ENC_LAST
+    return o;
+}
+
+// ---- decryption: FIPS-197 §5.3.5 equivalent inverse cipher ------------------
+// Input s already XORed with dk[0] (= w[Nr]).  Returns the state after the
+// final AddRoundKey (dk[Nr] = w[0]); the CBC XOR is applied by the caller.
+template <int NR>
+__device__ __forceinline__ uint4 decrypt_rounds(const char *sm, uint32_t lb, uint4 s, const RoundKeys &dk) {
+    uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+        const uint32_t t0 = T<0>(sm, s0, lb) ^ T<1>(sm, s3, lb) ^ T<2>(sm, s2, lb) ^ T<3>(sm, s1, lb) ^ dk.w[4 * r + 0];
+        const uint32_t t1 = T<0>(sm, s1, lb) ^ T<1>(sm, s0, lb) ^ T<2>(sm, s3, lb) ^ T<3>(sm, s2, lb) ^ dk.w[4 * r + 1];
+        const uint32_t t2 = T<0>(sm, s2, lb) ^ T<1>(sm, s1, lb) ^ T<2>(sm, s0, lb) ^ T<3>(sm, s3, lb) ^ dk.w[4 * r + 2];
+        const uint32_t t3 = T<0>(sm, s3, lb) ^ T<1>(sm, s2, lb) ^ T<2>(sm, s1, lb) ^ T<3>(sm, s0, lb) ^ dk.w[4 * r + 3];
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    uint4 o;
+#define KG_DEC_LAST(dst, a, b, c, d, kw)                                                                  \
+    dst = __byte_perm(__byte_perm(IS<0>(sm, a, lb), IS<1>(sm, b, lb), 0x0040u),                           \
+                      __byte_perm(IS<2>(sm, c, lb), IS<3>(sm, d, lb), 0x4000u), 0x7610u) ^ dk.w[4 * NR + kw];
+    KG_DEC_LAST(o.x, s0, s3, s2, s1, 0)
+    KG_DEC_LAST(o.y, s1, s0, s3, s2, 1)
+    KG_DEC_LAST(o.z, s2, s1, s0, s3, 2)
+    KG_DEC_LAST(o.w, s3, s2, s1, s0, 3)
+#undef KG_DEC_LAST
+    return o;
+}
+
+__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
+    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+}
+
+__device__ __forceinline__ uint4 xor4k(uint4 a, const RoundKeys &k, int r) {
+    return make_uint4(a.x ^ k.w[4 * r], a.y ^ k.w[4 * r + 1], a.z ^ k.w[4 * r + 2], a.w ^ k.w[4 * r + 3]);
+}
+
+__device__ __forceinline__ uint4 shfl4(uint4 v, int src) {
+    return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                      __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+
+__device__ __forceinline__ uint4 shfl_up4(uint4 v) {
+    return make_uint4(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1),
+                      __shfl_up_sync(0xffffffffu, v.z, 1), __shfl_up_sync(0xffffffffu, v.w, 1));
+}
+
+// Balanced split of [0, n) into g parts: start of part k.
+__device__ __forceinline__ uint64_t part_start(uint64_t n, uint64_t g, uint64_t k) {
+    const uint64_t q = n / g, r = n % g;
+    return k * q + (k < r ? k : r);
+}
+
+__device__ __forceinline__ uint32_t lane_bytes() {
+    const uint32_t l4 = (threadIdx.x & 31) * 4;
+    return l4 | ((128u + l4) << 8);
+}
+
+// ---- block-parallel kernel: CBC decrypt, ECB decrypt, ECB encrypt -----------
+template <int NR, int DIR, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant__ LaunchArgs a) {
+    extern __shared__ __align__(16) char sm[];
+    constexpr bool DEC = (DIR == 1);
+    constexpr bool CBC = (MODE == 0);
+    fill_tables<DEC>(sm);
+
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t lb = lane_bytes();
+    const uint64_t m = a.m;
+
+    // CTA range [c0, c1) of blocks: whole pages when in place (see header).
+    uint64_t c0, c1;
+    if (a.in_place) {
+        c0 = part_start(a.n_pages, gridDim.x, blockIdx.x) * m;
+        c1 = part_start(a.n_pages, gridDim.x, blockIdx.x + 1) * m;
+    } else {
+        const uint64_t nb = a.n_pages * m;
+        c0 = part_start(nb, gridDim.x, blockIdx.x);
+        c1 = part_start(nb, gridDim.x, blockIdx.x + 1);
+    }
+    const uint64_t w0 = c0 + part_start(c1 - c0, nwarps, warp);
+    const uint64_t w1 = c0 + part_start(c1 - c0, nwarps, warp + 1);
+
+    // Per-lane position of block g = w0 + lane: page and index j in page.
+    uint64_t page = (w0 + lane) / m;
+    uint32_t j = (uint32_t)((w0 + lane) - page * m);
+
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    if (CBC && DEC) {
+        // Snapshot the predecessor of this warp's first block before anyone
+        // in the CTA stores (in-place safety).
+        if (w0 < w1 && (w0 % m) != 0) carry = a.in[w0 - 1];
+    }
+    __syncthreads();
+
+    for (uint64_t u = w0; u < w1; u += 32) {
+        const uint64_t g = u + lane;
+        const bool act = g < w1;
+        const uint4 c = act ? a.in[g] : make_uint4(0, 0, 0, 0);
+        uint4 prev = make_uint4(0, 0, 0, 0);
+        if (CBC && DEC) {
+            const uint4 up = shfl_up4(c);
+            const uint4 last = shfl4(c, 31);
+            prev = (lane == 0) ? carry : up;
+            if (act && j == 0) prev = a.ivs[page];
+            carry = last;
+        }
+        uint4 o;
+        if (DEC) {
+            o = decrypt_rounds<NR>(sm, lb, xor4k(c, a.rk, 0), a.rk);
+            if (CBC) o = xor4(o, prev);
+        } else {
+            o = encrypt_rounds<NR>(sm, lb, xor4k(c, a.rk, 0), a.rk);
+        }
+        if (act) a.out[g] = o;
+        // advance (page, j) by 32 blocks
+        j += 32;
+        if (j >= m) {
+            if (m >= 32) {
+                j -= (uint32_t)m;
+                ++page;
+            } else {
+                page += j / (uint32_t)m;
+                j %= (uint32_t)m;
+            }
+        }
+    }
+}
+
+// ---- chain kernel: CBC encrypt, one thread per page chain --------------------
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
+    extern __shared__ __align__(16) char sm[];
+    fill_tables<false>(sm);
+    __syncthreads();
+    const uint32_t lb = lane_bytes();
+    const uint32_t m = a.m;
+    const uint64_t p0 = part_start(a.n_pages, gridDim.x, blockIdx.x);
+    const uint64_t p1 = part_start(a.n_pages, gridDim.x, blockIdx.x + 1);
+    for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const uint4 *src = a.in + p * m;
+        uint4 *dst = a.out + p * m;
+        uint4 prev = a.ivs[p];  // C_{p,-1} := IV_p
+        uint4 x = src[0];
+        for (uint32_t j = 0; j < m; ++j) {
+            uint4 xn = x;
+            if (j + 1 < m) xn = src[j + 1];  // prefetch P_{j+1} (read before C_j is stored)
+            // C_j = E_K(P_j ^ C_{j-1}); the first AddRoundKey folds into the same XOR
+            prev = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x, prev), a.rk, 0), a.rk);
+            dst[j] = prev;
+            x = xn;
+        }
+    }
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, int bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+template <int NR>
+cudaError_t init_nr() {
+    cudaError_t e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 0>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 1>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 0, 1>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_cbc_enc<NR>, kSmemEnc)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+template <int NR>
+cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaStream_t st) {
+    const uint64_t nb = a.n_pages * (uint64_t)a.m;
+    if (dir == 0 && mode == 0) {
+        const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
+        kg_cbc_enc<NR><<<grid, kThreads, kSmemEnc, st>>>(a);
+        return cudaGetLastError();
+    }
+    uint64_t want = (nb + 255) / 256;
+    if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
+    if (a.in_place && want > a.n_pages) want = a.n_pages;
+    if (want < 1) want = 1;
+    const unsigned grid = (unsigned)want;
+    if (dir == 1 && mode == 0) kg_blockpar<NR, 1, 0><<<grid, kThreads, kSmemDec, st>>>(a);
+    else if (dir == 1) kg_blockpar<NR, 1, 1><<<grid, kThreads, kSmemDec, st>>>(a);
+    else kg_blockpar<NR, 0, 1><<<grid, kThreads, kSmemEnc, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t kernels_init(const BaseTables &t) {
+    cudaError_t e = cudaMemcpyToSymbol(g_tables, &t, sizeof(BaseTables));
+    if (e != cudaSuccess) return e;
+    if ((e = init_nr<10>()) != cudaSuccess) return e;
+    if ((e = init_nr<12>()) != cudaSuccess) return e;
+    return init_nr<14>();
+}
+
+cudaError_t launch_pages(int dir, int mode, int nr, const LaunchArgs &a, int num_sms, cudaStream_t st) {
+    switch (nr) {
+        case 10: return launch_nr<10>(dir, mode, a, num_sms, st);
+        case 12: return launch_nr<12>(dir, mode, a, num_sms, st);
+        case 14: return launch_nr<14>(dir, mode, a, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace kg
