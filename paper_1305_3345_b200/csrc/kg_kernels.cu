@@ -140,9 +140,21 @@ __device__ __forceinline__ uint4 shfl4(uint4 v, int src) {
                       __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
 }
 
-__device__ __forceinline__ uint4 shfl_up4(uint4 v) {
-    return make_uint4(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1),
-                      __shfl_up_sync(0xffffffffu, v.z, 1), __shfl_up_sync(0xffffffffu, v.w, 1));
+// Streaming 128-bit global access (each byte is touched exactly once).
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(uint4 *p, uint4 v) { __stcs(p, v); }
+
+// 256-bit (two-block) global access: LDG.E.ENL2.256 / STG.E.ENL2.256 on
+// sm_100.  One L1 wavefront moves two blocks of a page chain instead of one.
+__device__ __forceinline__ void ld256(const uint4 *p, uint4 &a, uint4 &b) {
+    asm volatile("ld.global.cs.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(uint4 *p, uint4 a, uint4 b) {
+    asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+                 "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
 }
 
 // Balanced split of [0, n) into g parts: start of part k.
@@ -191,19 +203,24 @@ __global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant
         // in the CTA stores (in-place safety).
         if (w0 < w1 && (w0 % m) != 0) carry = a.in[w0 - 1];
     }
+    // Software pipeline: the next unit's ciphertext is in flight while the
+    // current unit's rounds run (hides the HBM latency behind the lookups).
+    uint4 c_next = (w0 + lane < w1) ? ld_stream(a.in + w0 + lane) : make_uint4(0, 0, 0, 0);
     __syncthreads();
 
     for (uint64_t u = w0; u < w1; u += 32) {
         const uint64_t g = u + lane;
         const bool act = g < w1;
-        const uint4 c = act ? a.in[g] : make_uint4(0, 0, 0, 0);
+        const uint4 c = c_next;
+        c_next = (g + 32 < w1) ? ld_stream(a.in + g + 32) : make_uint4(0, 0, 0, 0);
         uint4 prev = make_uint4(0, 0, 0, 0);
         if (CBC && DEC) {
-            const uint4 up = shfl_up4(c);
-            const uint4 last = shfl4(c, 31);
-            prev = (lane == 0) ? carry : up;
+            // rotate by one lane: lane L gets C of lane L-1; lane 0 gets this
+            // unit's lane 31, which is the next unit's lane-0 predecessor.
+            const uint4 r = shfl4(c, (lane + 31) & 31);
+            prev = (lane == 0) ? carry : r;
+            carry = r;
             if (act && j == 0) prev = a.ivs[page];
-            carry = last;
         }
         uint4 o;
         if (DEC) {
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant
         } else {
             o = encrypt_rounds<NR>(sm, lb, xor4k(c, a.rk, 0), a.rk);
         }
-        if (act) a.out[g] = o;
+        if (act) st_stream(a.out + g, o);
         // advance (page, j) by 32 blocks
         j += 32;
         if (j >= m) {
@@ -228,7 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant
 }
 
 // ---- chain kernel: CBC encrypt, one thread per page chain --------------------
-template <int NR>
+// WIDE (m even): blocks move two at a time with 256-bit loads/stores.
+template <int NR, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
     fill_tables<false>(sm);
@@ -241,14 +259,28 @@ __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant_
         const uint4 *src = a.in + p * m;
         uint4 *dst = a.out + p * m;
         uint4 prev = a.ivs[p];  // C_{p,-1} := IV_p
-        uint4 x = src[0];
-        for (uint32_t j = 0; j < m; ++j) {
-            uint4 xn = x;
-            if (j + 1 < m) xn = src[j + 1];  // prefetch P_{j+1} (read before C_j is stored)
-            // C_j = E_K(P_j ^ C_{j-1}); the first AddRoundKey folds into the same XOR
-            prev = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x, prev), a.rk, 0), a.rk);
-            dst[j] = prev;
-            x = xn;
+        if (WIDE) {
+            uint4 x0, x1;
+            ld256(src, x0, x1);
+            for (uint32_t j = 0; j < m; j += 2) {
+                uint4 n0 = x0, n1 = x1;
+                if (j + 2 < m) ld256(src + j + 2, n0, n1);  // prefetch P_{j+2}, P_{j+3}
+                // C_j = E_K(P_j ^ C_{j-1}); the first AddRoundKey folds into the same XOR
+                const uint4 c0 = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x0, prev), a.rk, 0), a.rk);
+                prev = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x1, c0), a.rk, 0), a.rk);
+                st256(dst + j, c0, prev);
+                x0 = n0;
+                x1 = n1;
+            }
+        } else {
+            uint4 x = src[0];
+            for (uint32_t j = 0; j < m; ++j) {
+                uint4 xn = x;
+                if (j + 1 < m) xn = src[j + 1];  // prefetch P_{j+1} (read before C_j is stored)
+                prev = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x, prev), a.rk, 0), a.rk);
+                dst[j] = prev;
+                x = xn;
+            }
         }
     }
 }
@@ -264,7 +296,8 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_blockpar<NR, 1, 0>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_blockpar<NR, 1, 1>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_blockpar<NR, 0, 1>, kSmemEnc)) != cudaSuccess) return e;
-    if ((e = set_smem(kg_cbc_enc<NR>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_cbc_enc<NR, true>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_cbc_enc<NR, false>, kSmemEnc)) != cudaSuccess) return e;
     return cudaSuccess;
 }
 
@@ -273,7 +306,8 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     if (dir == 0 && mode == 0) {
         const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
-        kg_cbc_enc<NR><<<grid, kThreads, kSmemEnc, st>>>(a);
+        if ((a.m & 1) == 0) kg_cbc_enc<NR, true><<<grid, kThreads, kSmemEnc, st>>>(a);
+        else kg_cbc_enc<NR, false><<<grid, kThreads, kSmemEnc, st>>>(a);
         return cudaGetLastError();
     }
     uint64_t want = (nb + 255) / 256;
