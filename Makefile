@@ -7,7 +7,7 @@ PKG     := paper_1305_3345_b200
 CSRC    := $(PKG)/csrc
 LIB     := $(PKG)/libkgpu.so
 
-all: $(LIB) oracle/libkgo.so build/test_kat build/pipes
+all: $(LIB) oracle/libkgo.so build/test_kat build/pipes build/latency
 
 build:
 	mkdir -p build
@@ -31,6 +31,9 @@ build/test_kat: oracle/kgo_aes.c oracle/kgo_pages.c oracle/test_kat.c oracle/kgo
 # pipe microbenchmarks (roofline inputs)
 build/pipes: tools/pipes.cu | build
 	$(NVCC) -O3 -lineinfo -std=c++17 $(ARCH) -o $@ $<
+
+build/latency: tools/latency.cu include/kg.h $(LIB) | build
+	$(NVCC) -O2 -std=c++17 $(ARCH) -Iinclude -o $@ $< -L$(PKG) -lkgpu -Xlinker -rpath,'$$ORIGIN/../$(PKG)'
 
 clean:
 	rm -rf build $(LIB) oracle/libkgo.so

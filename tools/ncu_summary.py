@@ -37,6 +37,11 @@ KEYS = [
     "smsp__pcsamp_warps_issue_stalled_wait", "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle",
     "smsp__pcsamp_warps_issue_stalled_barrier", "smsp__pcsamp_warps_issue_stalled_dispatch_stall",
     "smsp__pcsamp_sample_count",
+    "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg", "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_lgds.avg",
+    "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts_mem_shared.avg", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_st.sum",
+    "memory_l1_wavefronts_shared", "memory_l1_wavefronts_shared_ideal", "smsp__inst_executed.sum",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -71,7 +76,7 @@ def main():
                 t = float(d["gpu__time_duration.sum"].replace(",", ""))
                 unit = u.get("gpu__time_duration.sum", "ns")
                 scale = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "nsecond": 1e-9, "msecond": 1e-3, "ms": 1e-3}.get(unit, 1e-9)
-                rec["payload_GBps_at_ncu_time"] = a.payload / (t * scale) / 1e9
+                rec["payload_GBps_at_ncu_time"] = (f"{a.payload / (t * scale) / 1e9:.2f}", "GB/s")
             except (KeyError, ValueError):
                 pass
         recs.append(rec)
