@@ -145,6 +145,20 @@ KG_API const char *kg_strerror(int status);
  * kg_init: KG_CHUNK_BYTES, KG_STAGING_SLOTS.  KG_EINVAL on bad values. */
 KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);
 
+/* How batches touching pinned host memory reach the GPU (rows a3/a8 vs f4):
+ *   KG_HOST_STAGED   copy engines move chunks through the device staging ring
+ *                    (H2D || kernel || D2H on three streams; default);
+ *   KG_HOST_ZEROCOPY the kernel reads and writes the caller's pinned pages
+ *                    directly over the host link (no copies, one launch) --
+ *                    the paper's §4 "save an extra copy" idea;
+ *   KG_HOST_AUTO     zero-copy for batches of at most zc_max_bytes, staged above.
+ * Takes effect for later submits.  Environment override at kg_init:
+ * KG_HOST_PATH=0|1|2.  Errors: KG_ENOTINIT, KG_EINVAL (bad mode). */
+#define KG_HOST_STAGED 0
+#define KG_HOST_ZEROCOPY 1
+#define KG_HOST_AUTO 2
+KG_API int kg_set_host_path(int mode, uint64_t zc_max_bytes);
+
 /* Number of CUDA kernels this library has launched in this process
  * (instrumentation for benchmarks; monotonic, never reset). */
 KG_API uint64_t kg_launch_count(void);

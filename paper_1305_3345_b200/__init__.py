@@ -25,7 +25,8 @@ MAX_INFLIGHT = 65536
 
 #: every symbol include/kg.h declares
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
-               "kg_strerror", "kg_set_pipeline", "kg_launch_count")
+               "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path")
+HOST_STAGED, HOST_ZEROCOPY, HOST_AUTO = 0, 1, 2
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `make` (or __graft_entry__.build()); "
@@ -49,6 +50,8 @@ _lib.kg_strerror.argtypes = [ctypes.c_int]
 _lib.kg_strerror.restype = ctypes.c_char_p
 _lib.kg_set_pipeline.argtypes = [ctypes.c_uint64, ctypes.c_int]
 _lib.kg_set_pipeline.restype = ctypes.c_int
+_lib.kg_set_host_path.argtypes = [ctypes.c_int, ctypes.c_uint64]
+_lib.kg_set_host_path.restype = ctypes.c_int
 _lib.kg_launch_count.argtypes = []
 _lib.kg_launch_count.restype = ctypes.c_uint64
 
@@ -136,6 +139,10 @@ def shutdown() -> None:
 
 def set_pipeline(chunk_bytes: int, slots: int) -> None:
     _check(_lib.kg_set_pipeline(int(chunk_bytes), int(slots)), "kg_set_pipeline")
+
+
+def set_host_path(mode: int, zc_max_bytes: int = 1 << 20) -> None:
+    _check(_lib.kg_set_host_path(int(mode), int(zc_max_bytes)), "kg_set_host_path")
 
 
 def launch_count() -> int:

@@ -67,6 +67,8 @@ struct Ctx {
     int n_slots = 3;
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
+    int host_path = KG_HOST_STAGED;
+    uint64_t zc_max_bytes = 1ull << 20;
 };
 
 std::mutex g_mu;
@@ -138,7 +140,9 @@ int ensure_staging(uint64_t bytes, uint64_t ivb) {
 
 enum Kind { K_BAD = 0, K_DEVICE = 1, K_HOST = 2 };
 
-Kind classify(const void *p) {
+// Classify a caller pointer; for pinned host memory also return the address
+// a kernel may use to reach it over the host link (UVA: usually identical).
+Kind classify(const void *p, const void **dev_alias = nullptr) {
     cudaPointerAttributes at;
     cudaError_t e = cudaPointerGetAttributes(&at, p);
     if (e != cudaSuccess) {
@@ -151,6 +155,13 @@ Kind classify(const void *p) {
         case cudaMemoryTypeManaged:
             return K_DEVICE;
         case cudaMemoryTypeHost:
+            if (dev_alias) {
+                // devicePointer is the mapping of the allocation's base address
+                *dev_alias = at.devicePointer
+                                 ? (const void *)((const uint8_t *)at.devicePointer +
+                                                  ((const uint8_t *)p - (const uint8_t *)at.hostPointer))
+                                 : nullptr;
+            }
             return K_HOST;
         default:
             return K_BAD;  // unregistered (pageable) host memory
@@ -283,6 +294,10 @@ int kg_init(int device) {
         unsigned long long v = strtoull(e, nullptr, 0);
         if (v >= 16) g.chunk_bytes = v;
     }
+    if (const char *e = getenv("KG_HOST_PATH")) {
+        int v = atoi(e);
+        if (v >= KG_HOST_STAGED && v <= KG_HOST_AUTO) g.host_path = v;
+    }
     if (const char *e = getenv("KG_STAGING_SLOTS")) {
         int v = atoi(e);
         if (v >= 2 && v <= kMaxSlots) g.n_slots = v;
@@ -303,6 +318,15 @@ int kg_set_pipeline(uint64_t chunk_bytes, int slots) {
         g.n_slots = slots;
     }
     g.chunk_bytes = chunk_bytes;
+    return KG_OK;
+}
+
+int kg_set_host_path(int mode, uint64_t zc_max_bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.up) return KG_ENOTINIT;
+    if (mode != KG_HOST_STAGED && mode != KG_HOST_ZEROCOPY && mode != KG_HOST_AUTO) return KG_EINVAL;
+    g.host_path = mode;
+    g.zc_max_bytes = zc_max_bytes;
     return KG_OK;
 }
 
@@ -337,18 +361,26 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
     if (key_id < 0 || key_id >= KG_MAX_KEYS) return KG_EINVAL;
     const KeySlot &ks = g.keys[key_id];
     if (!ks.set) return KG_ENOKEY;
-    const Kind kin = classify(in), kout = classify(out), kiv = need_iv ? classify(ivs) : K_DEVICE;
+    const void *zin = in, *zout = out, *ziv = ivs;
+    const Kind kin = classify(in, &zin), kout = classify(out, &zout),
+               kiv = need_iv ? classify(ivs, &ziv) : K_DEVICE;
     if (kin == K_BAD || kout == K_BAD || kiv == K_BAD) return KG_EINVAL;
     if (g.tickets.size() >= (size_t)KG_MAX_INFLIGHT) return KG_EAGAIN;
 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const kg::RoundKeys &rk = (dir == KG_ENCRYPT) ? ks.enc : ks.dec;  // snapshot: copied into LaunchArgs
     int rc;
-    if (kin == K_DEVICE && kout == K_DEVICE && kiv == K_DEVICE) {
+    const bool all_device = (kin == K_DEVICE && kout == K_DEVICE && kiv == K_DEVICE);
+    // Zero-copy (row f4): the kernel reads and writes the
+    // caller's pinned pages over the host link, no staging copies.
+    const bool zero_copy = !all_device && zin && zout && (!need_iv || ziv) &&
+                           (g.host_path == KG_HOST_ZEROCOPY ||
+                            (g.host_path == KG_HOST_AUTO && total <= g.zc_max_bytes));
+    if (all_device || zero_copy) {
         kg::LaunchArgs a;
-        a.in = reinterpret_cast<const uint4 *>(in);
-        a.out = reinterpret_cast<uint4 *>(out);
-        a.ivs = need_iv ? reinterpret_cast<const uint4 *>(ivs) : nullptr;
+        a.in = reinterpret_cast<const uint4 *>(zin);
+        a.out = reinterpret_cast<uint4 *>(const_cast<void *>(zout));
+        a.ivs = need_iv ? reinterpret_cast<const uint4 *>(ziv) : nullptr;
         a.n_pages = n_pages;
         a.m = page_bytes / 16;
         a.in_place = (in == out);

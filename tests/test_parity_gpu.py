@@ -93,3 +93,26 @@ def test_small_staging_chunks_many_slots():
         finally:
             kg.set_pipeline(8 << 20, 3)
         assert first_mismatch(got, exp) is None, (chunk, slots)
+
+
+@pytest.mark.parametrize("n,pb", [(1, 16), (16, 4096), (149, 4096), (1000, 512), (3000, 4096)])
+@pytest.mark.parametrize("direction", [0, 1])
+@pytest.mark.parametrize("mode", ["zerocopy", "auto"])
+def test_cbc_host_zero_copy(direction, n, pb, mode):
+    """Row f4: kernels reading/writing pinned host pages directly (no staging)."""
+    from gpu_util import kg_ready
+    kg, torch = kg_ready()
+    key = synth.make_key(16, seed=3 * n + pb)
+    data = synth.make_pages(n, pb, seed=n + 1)
+    ivs = synth.make_ivs(n, seed=n + 2)
+    exp = oracle_pages(direction, 0, key, data, n, pb, ivs)
+    kg.set_host_path(kg.HOST_ZEROCOPY if mode == "zerocopy" else kg.HOST_AUTO, 64 << 10)
+    try:
+        got = gpu_pages(direction, 0, key, data, n, pb, ivs, where="pinned")
+        got_ip = gpu_pages(direction, 0, key, data, n, pb, ivs, where="pinned", inplace=True)
+        got_mixed = gpu_pages(direction, 0, key, data, n, pb, ivs, where="pinned", out_where="device")
+    finally:
+        kg.set_host_path(kg.HOST_STAGED)
+    assert first_mismatch(got, exp) is None
+    assert first_mismatch(got_ip, exp) is None
+    assert first_mismatch(got_mixed, exp) is None
