@@ -140,7 +140,7 @@ KG_API const char *kg_strerror(int status);
 
 /* Staging pipeline for batches touching host memory: chunk size in bytes
  * (rounded down to whole pages, at least one page) and number of device
- * staging slots (2..8).  Takes effect for later submits.  Defaults: 8 MiB,
+ * staging slots (2..8).  Takes effect for later submits.  Defaults: 16 MiB,
  * 3 slots ("three buffers").  Environment overrides at
  * kg_init: KG_CHUNK_BYTES, KG_STAGING_SLOTS.  KG_EINVAL on bad values. */
 KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);

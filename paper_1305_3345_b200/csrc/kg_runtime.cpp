@@ -63,7 +63,7 @@ struct Ctx {
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_begin = nullptr;
     Slot slots[kMaxSlots];
-    uint64_t chunk_bytes = 8ull << 20;
+    uint64_t chunk_bytes = 16ull << 20;
     int n_slots = 3;
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
@@ -73,6 +73,45 @@ struct Ctx {
 
 std::mutex g_mu;
 Ctx g;
+
+// KG_TRACE=1: record a timing event after every staging stage of the next
+// host batch and print the per-chunk timeline (JSON, stderr) at its kg_wait.
+struct TraceEv {
+    uint64_t chunk;
+    char stage;  // 'b' begin, 'h' H2D done, 'k' kernel done, 'd' D2H done
+    cudaEvent_t ev;
+};
+std::vector<TraceEv> g_trace;
+bool trace_on() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("KG_TRACE");
+        v = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+void trace(uint64_t chunk, char stage, cudaStream_t st) {
+    if (!trace_on()) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    g_trace.push_back({chunk, stage, e});
+}
+void trace_dump() {
+    if (g_trace.empty()) return;
+    cudaEventSynchronize(g_trace.back().ev);
+    fprintf(stderr, "{\"kg_trace\": [");
+    for (size_t i = 0; i < g_trace.size(); i++) {
+        float ms = 0.f;
+        cudaEventSynchronize(g_trace[i].ev);
+        cudaEventElapsedTime(&ms, g_trace[0].ev, g_trace[i].ev);
+        fprintf(stderr, "%s[%llu, \"%c\", %.2f]", i ? ", " : "", (unsigned long long)g_trace[i].chunk,
+                g_trace[i].stage, ms * 1000.f);
+    }
+    fprintf(stderr, "]}\n");
+    for (auto &t : g_trace) cudaEventDestroy(t.ev);
+    g_trace.clear();
+}
 std::atomic<uint64_t> g_launches{0};
 
 bool debug_on() {
@@ -203,6 +242,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     if (rc != KG_OK) return rc;
 
     KG_CU(cudaEventRecord(g.ev_begin, st));
+    trace(0, 'b', st);
     KG_CU(cudaStreamWaitEvent(g.s_h2d, g.ev_begin, 0));
     KG_CU(cudaStreamWaitEvent(g.s_comp, g.ev_begin, 0));
     KG_CU(cudaStreamWaitEvent(g.s_d2h, g.ev_begin, 0));
@@ -218,6 +258,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         if (need_iv && kiv == K_HOST)
             KG_CU(cudaMemcpyAsync(s.ivs, ivs + 16 * p0, 16 * np, cudaMemcpyHostToDevice, g.s_h2d));
         KG_CU(cudaEventRecord(s.loaded, g.s_h2d));
+        trace(i, 'h', g.s_h2d);
         // compute stage
         KG_CU(cudaStreamWaitEvent(g.s_comp, s.loaded, 0));
         kg::LaunchArgs a;
@@ -231,10 +272,12 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         rc = launch(dir, mode, nr, a, g.s_comp);
         if (rc != KG_OK) return rc;
         KG_CU(cudaEventRecord(s.done, g.s_comp));
+        trace(i, 'k', g.s_comp);
         // D2H stage
         KG_CU(cudaStreamWaitEvent(g.s_d2h, s.done, 0));
         if (kout == K_HOST) KG_CU(cudaMemcpyAsync(out + off, s.data, nbytes, cudaMemcpyDeviceToHost, g.s_d2h));
         KG_CU(cudaEventRecord(s.freed, g.s_d2h));
+        trace(i, 'd', g.s_d2h);
     }
     // join: the caller's stream continues after the last D2H
     KG_CU(cudaEventRecord(g.ev_begin, g.s_d2h));
@@ -406,6 +449,7 @@ int kg_wait(int64_t ticket) {
     }
     cudaError_t e = cudaEventSynchronize(ev);
     std::lock_guard<std::mutex> lk(g_mu);
+    if (trace_on()) trace_dump();
     g.tickets.erase(ticket);
     g.ev_pool.push_back(ev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");

@@ -91,7 +91,7 @@ def test_small_staging_chunks_many_slots():
         try:
             got = gpu_pages(1, 0, key, data, n, pb, ivs, where="pinned")
         finally:
-            kg.set_pipeline(8 << 20, 3)
+            kg.set_pipeline(16 << 20, 3)
         assert first_mismatch(got, exp) is None, (chunk, slots)
 
 
