@@ -159,6 +159,31 @@ KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);
 #define KG_HOST_AUTO 2
 KG_API int kg_set_host_path(int mode, uint64_t zc_max_bytes);
 
+/* Non-Stop Kernel (row f3; §3.1, 403-408 §3.2).
+ * kg_nsk_start launches ONE persistent service kernel on `ctas` SMs (0 ->
+ * 16; at most the SM count) that keeps the AES tables resident in shared
+ * memory and polls a request ring in mapped pinned host memory ("we use
+ * pinned memory to pass these messages").  While it runs,
+ * every kg_submit_pages is posted to it as a message instead of launching a
+ * kernel; in/out/ivs may be device memory or pinned host memory (accessed
+ * in place over the host link).  Completion is posted to pinned memory and
+ * kg_wait busy-waits on it.
+ * flags: 0 (ordered) -- the doorbell is rung by `stream` itself
+ *   (cuStreamWriteValue64), so the request runs after earlier work on
+ *   `stream`, and later work on `stream` waits for it (cuStreamWaitValue64);
+ *   KG_NSK_DIRECT -- the host rings the doorbell at submit (lowest latency;
+ *   ordering with `stream` is then the caller's job).
+ * idle_ms: the kernel exits after this long without requests (0 -> 2000 ms)
+ * and is relaunched transparently by the next submit.  The NSK occupies its
+ * SMs; other kernels share the remaining ones.
+ * Errors: KG_ENOTINIT; KG_EINVAL (bad ctas/flags, already running);
+ * KG_ENOTSUP (stream memory operations unavailable, ordered mode);
+ * KG_ENOMEM; KG_ECUDA.  kg_nsk_stop drains and stops it (KG_OK if not
+ * running); kg_shutdown stops it too. */
+#define KG_NSK_DIRECT 1
+KG_API int kg_nsk_start(int ctas, int flags, uint32_t idle_ms);
+KG_API int kg_nsk_stop(void);
+
 /* Number of CUDA kernels this library has launched in this process
  * (instrumentation for benchmarks; monotonic, never reset). */
 KG_API uint64_t kg_launch_count(void);

@@ -25,7 +25,9 @@ MAX_INFLIGHT = 65536
 
 #: every symbol include/kg.h declares
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
-               "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path")
+               "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path",
+               "kg_nsk_start", "kg_nsk_stop")
+NSK_DIRECT = 1
 HOST_STAGED, HOST_ZEROCOPY, HOST_AUTO = 0, 1, 2
 
 if not os.path.exists(LIB_PATH):
@@ -52,6 +54,10 @@ _lib.kg_set_pipeline.argtypes = [ctypes.c_uint64, ctypes.c_int]
 _lib.kg_set_pipeline.restype = ctypes.c_int
 _lib.kg_set_host_path.argtypes = [ctypes.c_int, ctypes.c_uint64]
 _lib.kg_set_host_path.restype = ctypes.c_int
+_lib.kg_nsk_start.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint32]
+_lib.kg_nsk_start.restype = ctypes.c_int
+_lib.kg_nsk_stop.argtypes = []
+_lib.kg_nsk_stop.restype = ctypes.c_int
 _lib.kg_launch_count.argtypes = []
 _lib.kg_launch_count.restype = ctypes.c_uint64
 
@@ -143,6 +149,15 @@ def set_pipeline(chunk_bytes: int, slots: int) -> None:
 
 def set_host_path(mode: int, zc_max_bytes: int = 1 << 20) -> None:
     _check(_lib.kg_set_host_path(int(mode), int(zc_max_bytes)), "kg_set_host_path")
+
+
+def nsk_start(ctas: int = 0, flags: int = 0, idle_ms: int = 0) -> None:
+    """Start the Non-Stop Kernel (persistent service kernel, row f3)."""
+    _check(_lib.kg_nsk_start(int(ctas), int(flags), int(idle_ms)), "kg_nsk_start")
+
+
+def nsk_stop() -> None:
+    _check(_lib.kg_nsk_stop(), "kg_nsk_stop")
 
 
 def launch_count() -> int:

@@ -39,6 +39,38 @@ struct BaseTables {
     uint32_t isb4[256];   // Si(x) * 0x01010101
 };
 
+// ---- Non-Stop Kernel (NSK, row f3) ---------------------------
+// A persistent service kernel polls a request ring in host-mapped pinned
+// memory ("We use pinned memory to pass these messages"),
+// runs each request on all of its CTAs, and posts a completion back into the
+// same pinned memory.  Layout shared by kg_runtime.cpp and kg_kernels.cu.
+constexpr int kNskSlots = 64;
+constexpr uint32_t kNskOpQuit = 0xFFFFu;
+
+struct NskReq {            // written by the host, read by the NSK
+    uint64_t in, out, ivs; // device-usable addresses (device memory or mapped pinned host memory)
+    uint64_t n_pages;
+    uint32_t m;            // blocks per page
+    uint32_t op;           // dir | mode << 1, or kNskOpQuit
+    uint32_t nr;
+    uint32_t in_place;
+    uint32_t rk[60];       // round keys of the request's direction (RoundKeys layout)
+};
+
+struct NskRing {                      // host-mapped pinned memory
+    uint64_t doorbell[kNskSlots];     // = seq when request seq is posted (host store or cuStreamWriteValue64)
+    uint64_t done[kNskSlots];         // = seq when request seq has completed (NSK store, system scope)
+    uint64_t posted;                  // highest seq the host has handed out (idle watchdog guard)
+    uint64_t pad[7];
+    NskReq req[kNskSlots];
+};
+
+struct NskCtl {                       // device memory, private to the NSK
+    unsigned long long work_seq;      // CTA 0 -> all CTAs: request `work_seq` is ready in req[]
+    unsigned int done_count[kNskSlots];
+    NskReq req[kNskSlots];            // CTA 0's copy of the host request (read from L2 by all CTAs)
+};
+
 // kg_tables.cpp
 void build_base_tables(BaseTables *t);
 int expand_key(const uint8_t *key, int key_bytes, RoundKeys *enc, RoundKeys *dec);  // returns Nr or -1
@@ -47,5 +79,8 @@ int expand_key(const uint8_t *key, int key_bytes, RoundKeys *enc, RoundKeys *dec
 cudaError_t kernels_init(const BaseTables &t);
 // Enqueue one batch on `st`.  dir/mode/nr validated by the caller.
 cudaError_t launch_pages(int dir, int mode, int nr, const LaunchArgs &a, int num_sms, cudaStream_t st);
+// Launch the NSK cooperatively with `ctas` CTAs; it expects request seq0 next
+// and exits after idle_ns without a posted request (or on a quit request).
+cudaError_t launch_nsk(NskRing *ring_dev, NskCtl *ctl, uint64_t seq0, uint64_t idle_ns, int ctas, cudaStream_t st);
 
 }  // namespace kg

@@ -168,27 +168,55 @@ __device__ __forceinline__ uint32_t lane_bytes() {
     return l4 | ((128u + l4) << 8);
 }
 
-// ---- block-parallel kernel: CBC decrypt, ECB decrypt, ECB encrypt -----------
-template <int NR, int DIR, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant__ LaunchArgs a) {
-    extern __shared__ __align__(16) char sm[];
-    constexpr bool DEC = (DIR == 1);
-    constexpr bool CBC = (MODE == 0);
-    fill_tables<DEC>(sm);
+// ---- cipher policies -----------------------------------------------------------
+// first(x) = x ^ round key 0; rounds(s) = the remaining Nr rounds (through the
+// final AddRoundKey).  Param*: keys by value in the kernel parameter (constant
+// bank operands).  The NSK (kg_nsk.cuh) supplies shared-memory-key policies.
+template <int NR>
+struct ParamEnc {
+    const char *sm;
+    uint32_t lb;
+    const RoundKeys &k;
+    __device__ __forceinline__ uint4 first(uint4 x) const { return xor4k(x, k, 0); }
+    __device__ __forceinline__ uint4 rounds(uint4 s) const { return encrypt_rounds<NR>(sm, lb, s, k); }
+};
+template <int NR>
+struct ParamDec {
+    const char *sm;
+    uint32_t lb;
+    const RoundKeys &k;
+    __device__ __forceinline__ uint4 first(uint4 x) const { return xor4k(x, k, 0); }
+    __device__ __forceinline__ uint4 rounds(uint4 s) const { return decrypt_rounds<NR>(sm, lb, s, k); }
+};
 
+// One batch (or one CTA's share of it): where the pages are.
+struct Job {
+    const uint4 *in;
+    uint4 *out;
+    const uint4 *ivs;
+    uint64_t n_pages;
+    uint32_t m;
+    uint32_t in_place;
+};
+
+// ---- block-parallel body: CBC decrypt, ECB decrypt, ECB encrypt ---------------
+// CTA `cta` of `ncta` processes its balanced share of the batch; each warp
+// streams a contiguous sub-range 32 blocks at a time.  Contains one
+// __syncthreads (all threads of the CTA must call it).
+template <bool DEC, bool CBC, class Cipher>
+__device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const uint32_t lb = lane_bytes();
     const uint64_t m = a.m;
 
     // CTA range [c0, c1) of blocks: whole pages when in place (see header).
     uint64_t c0, c1;
     if (a.in_place) {
-        c0 = part_start(a.n_pages, gridDim.x, blockIdx.x) * m;
-        c1 = part_start(a.n_pages, gridDim.x, blockIdx.x + 1) * m;
+        c0 = part_start(a.n_pages, ncta, cta) * m;
+        c1 = part_start(a.n_pages, ncta, cta + 1) * m;
     } else {
         const uint64_t nb = a.n_pages * m;
-        c0 = part_start(nb, gridDim.x, blockIdx.x);
-        c1 = part_start(nb, gridDim.x, blockIdx.x + 1);
+        c0 = part_start(nb, ncta, cta);
+        c1 = part_start(nb, ncta, cta + 1);
     }
     const uint64_t w0 = c0 + part_start(c1 - c0, nwarps, warp);
     const uint64_t w1 = c0 + part_start(c1 - c0, nwarps, warp + 1);
@@ -222,13 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant
             carry = r;
             if (act && j == 0) prev = a.ivs[page];
         }
-        uint4 o;
-        if (DEC) {
-            o = decrypt_rounds<NR>(sm, lb, xor4k(c, a.rk, 0), a.rk);
-            if (CBC) o = xor4(o, prev);
-        } else {
-            o = encrypt_rounds<NR>(sm, lb, xor4k(c, a.rk, 0), a.rk);
-        }
+        uint4 o = cph.rounds(cph.first(c));
+        if (CBC && DEC) o = xor4(o, prev);
         if (act) st_stream(a.out + g, o);
         // advance (page, j) by 32 blocks
         j += 32;
@@ -244,17 +267,13 @@ __global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant
     }
 }
 
-// ---- chain kernel: CBC encrypt, one thread per page chain --------------------
+// ---- chain body: CBC encrypt, one thread per page chain ------------------------
 // WIDE (m even): blocks move two at a time with 256-bit loads/stores.
-template <int NR, bool WIDE>
-__global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
-    extern __shared__ __align__(16) char sm[];
-    fill_tables<false>(sm);
-    __syncthreads();
-    const uint32_t lb = lane_bytes();
+template <bool WIDE, class Cipher>
+__device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
     const uint32_t m = a.m;
-    const uint64_t p0 = part_start(a.n_pages, gridDim.x, blockIdx.x);
-    const uint64_t p1 = part_start(a.n_pages, gridDim.x, blockIdx.x + 1);
+    const uint64_t p0 = part_start(a.n_pages, ncta, cta);
+    const uint64_t p1 = part_start(a.n_pages, ncta, cta + 1);
     for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const uint4 *src = a.in + p * m;
         uint4 *dst = a.out + p * m;
@@ -266,8 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant_
                 uint4 n0 = x0, n1 = x1;
                 if (j + 2 < m) ld256(src + j + 2, n0, n1);  // prefetch P_{j+2}, P_{j+3}
                 // C_j = E_K(P_j ^ C_{j-1}); the first AddRoundKey folds into the same XOR
-                const uint4 c0 = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x0, prev), a.rk, 0), a.rk);
-                prev = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x1, c0), a.rk, 0), a.rk);
+                const uint4 c0 = cph.rounds(cph.first(xor4(x0, prev)));
+                prev = cph.rounds(cph.first(xor4(x1, c0)));
                 st256(dst + j, c0, prev);
                 x0 = n0;
                 x1 = n1;
@@ -277,13 +296,46 @@ __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant_
             for (uint32_t j = 0; j < m; ++j) {
                 uint4 xn = x;
                 if (j + 1 < m) xn = src[j + 1];  // prefetch P_{j+1} (read before C_j is stored)
-                prev = encrypt_rounds<NR>(sm, lb, xor4k(xor4(x, prev), a.rk, 0), a.rk);
+                prev = cph.rounds(cph.first(xor4(x, prev)));
                 dst[j] = prev;
                 x = xn;
             }
         }
     }
 }
+
+__device__ __forceinline__ Job job_of(const LaunchArgs &a) {
+    Job j;
+    j.in = a.in;
+    j.out = a.out;
+    j.ivs = a.ivs;
+    j.n_pages = a.n_pages;
+    j.m = a.m;
+    j.in_place = a.in_place;
+    return j;
+}
+
+// ---- launch-per-batch kernels -------------------------------------------------
+template <int NR, int DIR, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant__ LaunchArgs a) {
+    extern __shared__ __align__(16) char sm[];
+    constexpr bool DEC = (DIR == 1);
+    constexpr bool CBC = (MODE == 0);
+    fill_tables<DEC>(sm);
+    const uint32_t lb = lane_bytes();
+    if (DEC) blockpar_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+    else blockpar_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+}
+
+template <int NR, bool WIDE>
+__global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
+    extern __shared__ __align__(16) char sm[];
+    fill_tables<false>(sm);
+    __syncthreads();
+    cbc_enc_body<WIDE>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
+}
+
+#include "kg_nsk.cuh"
 
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
@@ -326,6 +378,7 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
 cudaError_t kernels_init(const BaseTables &t) {
     cudaError_t e = cudaMemcpyToSymbol(g_tables, &t, sizeof(BaseTables));
     if (e != cudaSuccess) return e;
+    if ((e = set_smem(kg_nsk, kSmemNsk)) != cudaSuccess) return e;
     if ((e = init_nr<10>()) != cudaSuccess) return e;
     if ((e = init_nr<12>()) != cudaSuccess) return e;
     return init_nr<14>();
@@ -338,6 +391,11 @@ cudaError_t launch_pages(int dir, int mode, int nr, const LaunchArgs &a, int num
         case 14: return launch_nr<14>(dir, mode, a, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_nsk(NskRing *ring_dev, NskCtl *ctl, uint64_t seq0, uint64_t idle_ns, int ctas, cudaStream_t st) {
+    void *args[] = {&ring_dev, &ctl, &seq0, &idle_ns};
+    return cudaLaunchCooperativeKernel((const void *)kg_nsk, dim3(ctas), dim3(kThreads), args, kSmemNsk, st);
 }
 
 }  // namespace kg

@@ -17,6 +17,7 @@
 //  * There is no user-space helper process and no kernel module: one address
 //    space, so the copy engines DMA straight from/to the caller's pinned
 //    pages (the paper's own §4 "save an extra copy" idea).
+#include <cuda.h>  // driver API types only (entry points resolved at run time)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -40,9 +41,29 @@ struct KeySlot {
 };
 
 struct Ticket {
-    cudaEvent_t ev = nullptr;
+    cudaEvent_t ev = nullptr;     // launch/staged batches: completion event
     bool claimed = false;
+    uint64_t nsk_seq = 0;         // NSK requests: sequence number (ev == nullptr)
+    uint64_t nsk_gen = 0;         // NSK lifetime the request belongs to
 };
+
+// NSK state (row f3).  ring/ring_dev: host and device views of the mapped
+// pinned request ring.
+struct Nsk {
+    bool on = false;
+    int ctas = 0;
+    int flags = 0;
+    uint64_t idle_ns = 0;
+    kg::NskRing *ring = nullptr;
+    kg::NskRing *ring_dev = nullptr;
+    kg::NskCtl *ctl = nullptr;
+    cudaStream_t st = nullptr;
+    uint64_t seq = 0;            // last sequence number handed out
+    uint64_t gen = 0;            // incremented at every stop
+};
+
+typedef CUresult (*PFN_writeValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_waitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 
 struct Slot {
     uint8_t *data = nullptr;   // chunk_pages * page_bytes
@@ -69,6 +90,9 @@ struct Ctx {
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
     int host_path = KG_HOST_STAGED;
     uint64_t zc_max_bytes = 1ull << 20;
+    Nsk nsk;
+    PFN_writeValue64 write_value64 = nullptr;
+    PFN_waitValue64 wait_value64 = nullptr;
 };
 
 std::mutex g_mu;
@@ -113,6 +137,7 @@ void trace_dump() {
     g_trace.clear();
 }
 std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_nsk_waiters{0};
 
 bool debug_on() {
     static int v = -1;
@@ -285,6 +310,105 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     return KG_OK;
 }
 
+
+// ---- NSK host side ---------------------------------------------------------------
+inline uint64_t vload(const uint64_t *p) { return *reinterpret_cast<const volatile uint64_t *>(p); }
+inline void vstore(uint64_t *p, uint64_t v) { *reinterpret_cast<volatile uint64_t *>(p) = v; }
+inline void cpu_relax() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+}
+
+int nsk_launch(uint64_t seq0) {
+    KG_CU(cudaMemsetAsync(g.nsk.ctl, 0, sizeof(kg::NskCtl), g.nsk.st));
+    KG_CU(kg::launch_nsk(g.nsk.ring_dev, g.nsk.ctl, seq0, g.nsk.idle_ns, g.nsk.ctas, g.nsk.st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KG_OK;
+}
+
+// The NSK exits on its own after idle_ns without work; relaunch it then.
+int nsk_ensure_alive() {
+    cudaError_t e = cudaStreamQuery(g.nsk.st);
+    if (e == cudaErrorNotReady) {
+        cudaGetLastError();
+        return KG_OK;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "NSK died");
+    return nsk_launch(g.nsk.seq + 1);
+}
+
+// Block until ring slot of `seq` is free (its previous request completed).
+int nsk_slot_wait(uint64_t seq) {
+    if (seq <= (uint64_t)kg::kNskSlots) return KG_OK;
+    const int slot = (int)((seq - 1) % kg::kNskSlots);
+    const uint64_t need = seq - kg::kNskSlots;
+    for (uint64_t spin = 0; vload(&g.nsk.ring->done[slot]) < need; ++spin) {
+        cpu_relax();
+        if ((spin & 0xFFFFF) == 0xFFFFF) {
+            cudaError_t e = cudaStreamQuery(g.nsk.st);
+            if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_fail(e, "NSK died");
+        }
+    }
+    return KG_OK;
+}
+
+// Post one request; returns its sequence number (> 0) or a status (< 0).
+int64_t nsk_post(uint32_t op, const void *in, void *out, const void *ivs, uint64_t n_pages, uint32_t m,
+                 uint32_t in_place, int nr, const kg::RoundKeys *rk, cudaStream_t st, bool direct) {
+    int rc = nsk_ensure_alive();
+    if (rc != KG_OK) return rc;
+    const uint64_t seq = g.nsk.seq + 1;
+    rc = nsk_slot_wait(seq);
+    if (rc != KG_OK) return rc;
+    const int slot = (int)((seq - 1) % kg::kNskSlots);
+    kg::NskReq r;
+    memset(&r, 0, sizeof r);
+    r.in = (uint64_t)(uintptr_t)in;
+    r.out = (uint64_t)(uintptr_t)out;
+    r.ivs = (uint64_t)(uintptr_t)ivs;
+    r.n_pages = n_pages;
+    r.m = m;
+    r.op = op;
+    r.nr = (uint32_t)nr;
+    r.in_place = in_place;
+    if (rk) memcpy(r.rk, rk->w, sizeof r.rk);
+    memcpy((void *)&g.nsk.ring->req[slot], &r, sizeof r);
+    vstore(&g.nsk.ring->posted, seq);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    g.nsk.seq = seq;
+    if (direct) {
+        vstore(&g.nsk.ring->doorbell[slot], seq);
+    } else {
+        // ordered after earlier work on `st`; later work on `st` waits for completion
+        const CUdeviceptr bell = (CUdeviceptr)(uintptr_t)&g.nsk.ring_dev->doorbell[slot];
+        const CUdeviceptr done = (CUdeviceptr)(uintptr_t)&g.nsk.ring_dev->done[slot];
+        if (g.write_value64((CUstream)st, bell, seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return KG_ECUDA;
+        if (g.wait_value64((CUstream)st, done, seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) return KG_ECUDA;
+    }
+    return (int64_t)seq;
+}
+
+int nsk_stop_locked() {
+    if (!g.nsk.on) return KG_OK;
+    int rc = KG_OK;
+    if (cudaStreamQuery(g.nsk.st) == cudaErrorNotReady) {
+        cudaGetLastError();
+        const int64_t q = nsk_post(kg::kNskOpQuit, nullptr, nullptr, nullptr, 0, 1, 0, 10, nullptr, nullptr, true);
+        if (q < 0) rc = (int)q;
+    }
+    cudaError_t e = cudaStreamSynchronize(g.nsk.st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "NSK stop");
+    while (g_nsk_waiters.load() != 0) cpu_relax();  // waiters see their done word before the kernel exits
+    cudaFreeHost(g.nsk.ring);
+    cudaFree(g.nsk.ctl);
+    cudaStreamDestroy(g.nsk.st);
+    const uint64_t gen = g.nsk.gen + 1;
+    g.nsk = Nsk();
+    g.nsk.gen = gen;
+    return rc;
+}
 }  // namespace
 
 extern "C" {
@@ -332,6 +456,18 @@ int kg_init(int device) {
         KG_CU(cudaEventCreateWithFlags(&g.slots[i].loaded, cudaEventDisableTiming));
         KG_CU(cudaEventCreateWithFlags(&g.slots[i].done, cudaEventDisableTiming));
         KG_CU(cudaEventCreateWithFlags(&g.slots[i].freed, cudaEventDisableTiming));
+    }
+    {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g.write_value64 = (PFN_writeValue64)fn;
+        fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g.wait_value64 = (PFN_waitValue64)fn;
+        cudaGetLastError();
     }
     if (const char *e = getenv("KG_CHUNK_BYTES")) {
         unsigned long long v = strtoull(e, nullptr, 0);
@@ -413,6 +549,20 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const kg::RoundKeys &rk = (dir == KG_ENCRYPT) ? ks.enc : ks.dec;  // snapshot: copied into LaunchArgs
     int rc;
+    if (g.nsk.on) {
+        // Every request goes to the resident service kernel (it owns its SMs).
+        if (!zin || !zout || (need_iv && !ziv)) return KG_EINVAL;
+        const uint32_t op = (uint32_t)dir | ((uint32_t)mode << 1);
+        const int64_t seq = nsk_post(op, zin, const_cast<void *>(zout), need_iv ? ziv : nullptr, n_pages,
+                                     page_bytes / 16, in == out, ks.nr, &rk, st, (g.nsk.flags & KG_NSK_DIRECT) != 0);
+        if (seq < 0) return seq;
+        const int64_t t = g.next_ticket++;
+        Ticket tk;
+        tk.nsk_seq = (uint64_t)seq;
+        tk.nsk_gen = g.nsk.gen;
+        g.tickets[t] = tk;
+        return t;
+    }
     const bool all_device = (kin == K_DEVICE && kout == K_DEVICE && kiv == K_DEVICE);
     // Zero-copy (row f4): the kernel reads and writes the
     // caller's pinned pages over the host link, no staging copies.
@@ -437,8 +587,21 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
     return new_ticket(st);
 }
 
+// NSK ticket completion: 1 done, 0 pending, < 0 error.  Caller holds g_mu.
+int nsk_ticket_state(const Ticket &t) {
+    if (t.nsk_gen != g.nsk.gen || !g.nsk.on) return 1;  // the NSK was stopped after draining it
+    const int slot = (int)((t.nsk_seq - 1) % kg::kNskSlots);
+    if (vload(&g.nsk.ring->done[slot]) >= t.nsk_seq) return 1;
+    cudaError_t e = cudaStreamQuery(g.nsk.st);
+    if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_fail(e, "NSK died");
+    return 0;
+}
+
 int kg_wait(int64_t ticket) {
     cudaEvent_t ev;
+    Ticket nsk_ticket;
+    const uint64_t *done_word = nullptr;
+    cudaStream_t nsk_stream = nullptr;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         if (!g.up) return KG_ENOTINIT;
@@ -446,6 +609,36 @@ int kg_wait(int64_t ticket) {
         if (it == g.tickets.end() || it->second.claimed) return KG_ETICKET;
         it->second.claimed = true;
         ev = it->second.ev;
+        if (!ev) {
+            // NSK request: busy-wait on the pinned completion word (the paper's
+            // "busy-waiting on the response queue"), outside
+            // the lock; kg_nsk_stop waits for such waiters before freeing the ring.
+            nsk_ticket = it->second;
+            nsk_stream = g.nsk.st;
+            if (g.nsk.on && nsk_ticket.nsk_gen == g.nsk.gen) {
+                done_word = &g.nsk.ring->done[(nsk_ticket.nsk_seq - 1) % kg::kNskSlots];
+                g_nsk_waiters.fetch_add(1);
+            }
+        }
+    }
+    if (!ev) {
+        int rc = KG_OK;
+        if (done_word) {
+            for (uint64_t spin = 0; vload(done_word) < nsk_ticket.nsk_seq; ++spin) {
+                cpu_relax();
+                if ((spin & 0xFFFF) == 0xFFFF) {
+                    cudaError_t e = cudaStreamQuery(nsk_stream);
+                    if (e != cudaErrorNotReady && e != cudaSuccess) {
+                        rc = cuda_fail(e, "NSK died");
+                        break;
+                    }
+                }
+            }
+            g_nsk_waiters.fetch_sub(1);
+        }
+        std::lock_guard<std::mutex> lk(g_mu);
+        g.tickets.erase(ticket);
+        return rc;
     }
     cudaError_t e = cudaEventSynchronize(ev);
     std::lock_guard<std::mutex> lk(g_mu);
@@ -461,6 +654,7 @@ int kg_poll(int64_t ticket) {
     if (!g.up) return KG_ENOTINIT;
     auto it = g.tickets.find(ticket);
     if (it == g.tickets.end() || it->second.claimed) return KG_ETICKET;
+    if (!it->second.ev) return nsk_ticket_state(it->second);
     cudaError_t e = cudaEventQuery(it->second.ev);
     if (e == cudaSuccess) return 1;
     if (e == cudaErrorNotReady) {
@@ -470,11 +664,58 @@ int kg_poll(int64_t ticket) {
     return cuda_fail(e, "cudaEventQuery");
 }
 
+int kg_nsk_start(int ctas, int flags, uint32_t idle_ms) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.up) return KG_ENOTINIT;
+    if (flags & ~KG_NSK_DIRECT) return KG_EINVAL;
+    if (ctas == 0) ctas = 16;
+    if (ctas < 0 || ctas > g.num_sms) return KG_EINVAL;
+    if (g.nsk.on) return KG_EINVAL;
+    if (!(flags & KG_NSK_DIRECT) && (!g.write_value64 || !g.wait_value64)) return KG_ENOTSUP;
+    Nsk n;
+    n.ctas = ctas;
+    n.flags = flags;
+    n.idle_ns = (uint64_t)(idle_ms ? idle_ms : 2000) * 1000000ull;
+    n.gen = g.nsk.gen;
+    if (cudaHostAlloc((void **)&n.ring, sizeof(kg::NskRing), cudaHostAllocMapped) != cudaSuccess) {
+        cudaGetLastError();
+        return KG_ENOMEM;
+    }
+    memset(n.ring, 0, sizeof(kg::NskRing));
+    if (cudaHostGetDevicePointer((void **)&n.ring_dev, n.ring, 0) != cudaSuccess ||
+        cudaMalloc((void **)&n.ctl, sizeof(kg::NskCtl)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeHost(n.ring);
+        return KG_ENOMEM;
+    }
+    KG_CU(cudaStreamCreateWithFlags(&n.st, cudaStreamNonBlocking));
+    g.nsk = n;
+    g.nsk.on = true;
+    int rc = nsk_launch(1);
+    if (rc != KG_OK) {
+        cudaFreeHost(g.nsk.ring);
+        cudaFree(g.nsk.ctl);
+        cudaStreamDestroy(g.nsk.st);
+        const uint64_t gen = g.nsk.gen;
+        g.nsk = Nsk();
+        g.nsk.gen = gen;
+    }
+    return rc;
+}
+
+int kg_nsk_stop(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.up) return KG_ENOTINIT;
+    return nsk_stop_locked();
+}
+
 int kg_shutdown(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g.up) return KG_ENOTINIT;
+    nsk_stop_locked();
     cudaDeviceSynchronize();
-    for (auto &kv : g.tickets) cudaEventDestroy(kv.second.ev);
+    for (auto &kv : g.tickets)
+        if (kv.second.ev) cudaEventDestroy(kv.second.ev);
     g.tickets.clear();
     for (cudaEvent_t e : g.ev_pool) cudaEventDestroy(e);
     g.ev_pool.clear();

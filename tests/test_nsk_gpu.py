@@ -1,0 +1,136 @@
+"""Row f3: the Non-Stop Kernel (persistent service kernel).
+Parity with the oracle through the NSK in both doorbell modes, device and
+pinned-host buffers, ring wrap-around, idle exit + transparent relaunch,
+stream ordering, stop with outstanding tickets."""
+import time
+
+import numpy as np
+import pytest
+
+import synth
+from gpu_util import first_mismatch, kg_ready, oracle_pages, put
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def nsk():
+    kg, torch = kg_ready()
+    yield kg, torch
+    kg.nsk_stop()
+
+
+def run(kg, torch, direction, mode, key, data, n, pb, ivs, where, inplace=False, stream=None, key_id=0):
+    kg.set_key(key_id, key)
+    tin = put(torch, data, where)
+    tout = tin if inplace else (torch.empty_like(tin) if where == "device" else torch.empty_like(tin).pin_memory())
+    tiv = None if ivs is None else put(torch, ivs, where)
+    kg.wait(kg.submit_pages(direction, mode, tin, tout, n, pb, tiv, key_id, stream))
+    torch.cuda.synchronize()
+    return tout.cpu().numpy()
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+@pytest.mark.parametrize("where", ["device", "pinned"])
+def test_nsk_parity(nsk, flags, where):
+    kg, torch = nsk
+    kg.nsk_start(8, flags, 5000)
+    for (n, pb, kb) in [(1, 4096, 16), (16, 4096, 32), (33, 512, 24), (300, 4096, 16), (5, 16, 32), (1000, 48, 16)]:
+        key = synth.make_key(kb, seed=n + pb)
+        data = synth.make_pages(n, pb, seed=n * 7 + pb)
+        ivs = synth.make_ivs(n, seed=n * 11)
+        for d in (0, 1):
+            for mode in (0, 1):
+                exp = oracle_pages(d, mode, key, data, n, pb, ivs if mode == 0 else None)
+                got = run(kg, torch, d, mode, key, data, n, pb, ivs if mode == 0 else None, where)
+                assert first_mismatch(got, exp) is None, (n, pb, kb, d, mode)
+        got = run(kg, torch, 1, 0, key, exp if False else oracle_pages(0, 0, key, data, n, pb, ivs), n, pb, ivs,
+                  where, inplace=True)
+        assert np.array_equal(got, data)
+
+
+def test_nsk_ring_wraparound_and_many_inflight(nsk):
+    kg, torch = nsk
+    kg.nsk_start(4, kg.NSK_DIRECT, 5000)
+    n, pb = 4, 4096
+    key = synth.make_key(16, seed=1)
+    kg.set_key(0, key)
+    data = synth.make_pages(n, pb, seed=2)
+    ivs = synth.make_ivs(n, seed=3)
+    exp = oracle_pages(0, 0, key, data, n, pb, ivs)
+    src = torch.from_numpy(data).cuda()
+    iv = torch.from_numpy(ivs).cuda()
+    outs = [torch.empty_like(src) for _ in range(300)]
+    tickets = [kg.submit_pages(0, 0, src, o, n, pb, iv, 0) for o in outs]   # > 64 ring slots
+    assert all(b > a for a, b in zip(tickets, tickets[1:]))
+    for t in tickets:
+        kg.wait(t)
+    for o in outs[::37] + [outs[-1]]:
+        assert np.array_equal(o.cpu().numpy(), exp)
+
+
+def test_nsk_idle_exit_and_relaunch(nsk):
+    kg, torch = nsk
+    kg.nsk_start(2, kg.NSK_DIRECT, 30)        # 30 ms idle watchdog
+    key = synth.make_key(16, seed=9)
+    data = synth.make_pages(8, 4096, seed=10)
+    ivs = synth.make_ivs(8, seed=11)
+    exp = oracle_pages(1, 0, key, data, 8, 4096, ivs)
+    l0 = kg.launch_count()
+    for _ in range(3):
+        assert np.array_equal(run(kg, torch, 1, 0, key, data, 8, 4096, ivs, "device"), exp)
+        time.sleep(0.2)                        # the NSK exits; the next submit relaunches it
+    assert kg.launch_count() - l0 >= 2
+
+
+def test_nsk_stream_ordering(nsk):
+    """Ordered mode: the doorbell is rung by the stream after earlier work,
+    and later work on the stream sees the result."""
+    kg, torch = nsk
+    kg.nsk_start(8, 0, 5000)
+    n, pb = 2048, 4096
+    key = synth.make_key(16, seed=20)
+    kg.set_key(0, key)
+    p = torch.from_numpy(synth.make_pages(n, pb, seed=21)).cuda()
+    iv = torch.from_numpy(synth.make_ivs(n, seed=22)).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a = torch.zeros_like(p)
+        big = torch.ones(1 << 26, device="cuda")
+        for _ in range(10):
+            big.mul_(1.0001)
+        a.copy_(p)
+        c = torch.empty_like(a)
+        kg.submit_pages(0, 0, a, c, n, pb, iv, 0, stream=s)
+        back = torch.empty_like(a)
+        t = kg.submit_pages(1, 0, c, back, n, pb, iv, 0, stream=s)
+        ok = torch.equal(back, p)
+    kg.wait(t)
+    s.synchronize()
+    assert bool(ok)
+
+
+def test_nsk_stop_with_outstanding_and_restart(nsk):
+    kg, torch = nsk
+    kg.nsk_start(4, kg.NSK_DIRECT, 5000)
+    n, pb = 64, 4096
+    kg.set_key(0, synth.make_key(16, seed=30))
+    x = torch.from_numpy(synth.make_pages(n, pb, seed=31)).cuda()
+    iv = torch.from_numpy(synth.make_ivs(n, seed=32)).cuda()
+    y = torch.empty_like(x)
+    ts = [kg.submit_pages(0, 0, x, y, n, pb, iv, 0) for _ in range(10)]
+    kg.nsk_stop()
+    for t in ts:
+        kg.wait(t)                 # completed before the quit message
+    lib = kg.raw_lib()
+    assert lib.kg_nsk_stop() == kg.OK          # idempotent
+    assert lib.kg_nsk_start(10 ** 6, 0, 0) == kg.EINVAL
+    assert lib.kg_nsk_start(2, 8, 0) == kg.EINVAL
+    kg.nsk_start(2, 0, 0)
+    assert lib.kg_nsk_start(2, 0, 0) == kg.EINVAL   # already running
+    ref = torch.empty_like(x)
+    kg.wait(kg.submit_pages(0, 0, x, ref, n, pb, iv, 0))
+    kg.nsk_stop()
+    regular = torch.empty_like(x)
+    kg.wait(kg.submit_pages(0, 0, x, regular, n, pb, iv, 0))   # launch-per-batch path again
+    assert torch.equal(ref, regular) and torch.equal(y, regular)

@@ -93,6 +93,31 @@ int main(int argc, char **argv) {
         }
         report("kg_pinned_dec", v, pages);
     }
+    // the NSK (row f3): persistent service kernel, requests as messages in pinned memory
+    for (int flags : {KG_NSK_DIRECT, 0}) {
+        if (kg_nsk_start(16, flags, 5000) != KG_OK) {
+            printf("{\"error\": \"kg_nsk_start failed\"}\n");
+            continue;
+        }
+        for (int pages : {1, 16}) {
+            for (int pinned = 0; pinned < 2; pinned++) {
+                for (int pass = 0; pass < 2; pass++) {
+                    v.clear();
+                    for (int i = 0; i < reps; i++) {
+                        double t0 = now_us();
+                        int64_t t = pinned ? kg_submit_pages(KG_DECRYPT, KG_MODE_CBC, h_in, h_out, pages, PB, h_iv, 0, st)
+                                           : kg_submit_pages(KG_DECRYPT, KG_MODE_CBC, d_in, d_out, pages, PB, d_iv, 0, st);
+                        kg_wait(t);
+                        v.push_back(now_us() - t0);
+                    }
+                }
+                char name[96];
+                snprintf(name, sizeof name, "nsk_%s_%s_dec", flags ? "direct" : "ordered", pinned ? "pinned" : "hbm");
+                report(name, v, pages);
+            }
+        }
+        kg_nsk_stop();
+    }
     // submit-only cost (host side of the request queue)
     v.clear();
     std::vector<int64_t> ts;
