@@ -12,7 +12,7 @@ all: $(LIB) oracle/libkgo.so build/test_kat build/pipes build/latency
 build:
 	mkdir -p build
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/kg_internal.h include/kg.h | build
+build/%.o: $(CSRC)/%.cu $(CSRC)/kg_internal.h $(wildcard $(CSRC)/*.cuh) include/kg.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; false)
 
 build/%.o: $(CSRC)/%.cpp $(CSRC)/kg_internal.h include/kg.h | build

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 namespace kg {
@@ -47,7 +48,7 @@ struct BaseTables {
 constexpr int kNskSlots = 64;
 constexpr uint32_t kNskOpQuit = 0xFFFFu;
 
-struct NskReq {            // written by the host, read by the NSK
+struct alignas(16) NskReq {  // written by the host, read by the NSK (16-byte aligned: copied as uint4)
     uint64_t in, out, ivs; // device-usable addresses (device memory or mapped pinned host memory)
     uint64_t n_pages;
     uint32_t m;            // blocks per page
@@ -65,11 +66,15 @@ struct NskRing {                      // host-mapped pinned memory
     NskReq req[kNskSlots];
 };
 
+static_assert(sizeof(NskReq) % 16 == 0, "NskReq is copied as uint4");
+
 struct NskCtl {                       // device memory, private to the NSK
     unsigned long long work_seq;      // CTA 0 -> all CTAs: request `work_seq` is ready in req[]
     unsigned int done_count[kNskSlots];
     NskReq req[kNskSlots];            // CTA 0's copy of the host request (read from L2 by all CTAs)
+    uint64_t stamp[kNskSlots][8];     // %globaltimer per request (diagnostics, KG_NSK_STAMPS=1)
 };
+static_assert(offsetof(NskRing, req) % 16 == 0 && offsetof(NskCtl, req) % 16 == 0, "aligned request slots");
 
 // kg_tables.cpp
 void build_base_tables(BaseTables *t);

@@ -164,43 +164,52 @@ __device__ __forceinline__ void nsk_run(const Job &j, uint32_t op, const char *s
 __global__ void __launch_bounds__(kThreads, 1) kg_nsk(NskRing *ring, NskCtl *ctl, uint64_t seq0, uint64_t idle_ns) {
     extern __shared__ __align__(16) char sm[];
     uint4 *ks = reinterpret_cast<uint4 *>(sm + 3 * kRegion);
-    __shared__ NskReq cur;
+    __shared__ __align__(16) NskReq cur;
     fill_tables_nsk(sm);
     __syncthreads();
     const uint32_t lb = lane_bytes();
     for (uint64_t seq = seq0;; ++seq) {
         const int slot = (int)((seq - 1) % kNskSlots);
-        if (threadIdx.x == 0) {
-            if (blockIdx.x == 0) {
-                // poll the host doorbell for request `seq`
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+            // warp 0 of CTA 0: lane 0 polls the host doorbell for request `seq`,
+            // then the 18 uint4 of the request cross the host link in parallel.
+            int quit = 0;
+            if (threadIdx.x == 0) {
                 uint64_t t0 = globaltimer_ns();
-                bool quit = false;
                 while (ld_acquire_sys_u64(&ring->doorbell[slot]) != seq) {
                     if (globaltimer_ns() - t0 > idle_ns) {
                         if (ld_acquire_sys_u64(&ring->posted) >= seq) {
                             t0 = globaltimer_ns();  // handed out, doorbell pending: keep waiting
                         } else {
-                            quit = true;
+                            quit = 1;
                             break;
                         }
                     }
                     __nanosleep(64);
                 }
-                if (quit) {
-                    ctl->req[slot].op = kNskOpQuit;
-                } else {
-                    const uint4 *src = reinterpret_cast<const uint4 *>(&ring->req[slot]);
-                    uint4 *dst = reinterpret_cast<uint4 *>(&ctl->req[slot]);
-#pragma unroll
-                    for (int i = 0; i < (int)(sizeof(NskReq) / 16); i++) dst[i] = __ldcv(src + i);
-                }
-                __threadfence();
-                st_release_gpu_u64(&ctl->work_seq, seq);
-            } else {
-                while (ld_acquire_gpu_u64(&ctl->work_seq) < seq) __nanosleep(32);
             }
-            cur = ctl->req[slot];
+            if (threadIdx.x == 0) ctl->stamp[slot][0] = globaltimer_ns();  // doorbell seen
+            quit = __shfl_sync(0xffffffffu, quit, 0);
+            constexpr int kWords = (int)(sizeof(NskReq) / 16);
+            if (quit) {
+                if (threadIdx.x == 0) ctl->req[slot].op = kNskOpQuit;
+            } else if (threadIdx.x < kWords) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(&ring->req[slot]);
+                reinterpret_cast<uint4 *>(&ctl->req[slot])[threadIdx.x] = __ldcv(src + threadIdx.x);
+            }
+            __threadfence();
+            __syncwarp();
+            if (threadIdx.x == 0) {
+                ctl->stamp[slot][1] = globaltimer_ns();  // request copied to device memory
+                st_release_gpu_u64(&ctl->work_seq, seq);
+            }
+        } else if (threadIdx.x == 0) {
+            while (ld_acquire_gpu_u64(&ctl->work_seq) < seq) __nanosleep(32);
         }
+        __syncthreads();
+        // warp 0 pulls the request from L2 into shared memory, 16 bytes per lane
+        if (threadIdx.x < (int)(sizeof(NskReq) / 16))
+            reinterpret_cast<uint4 *>(&cur)[threadIdx.x] = reinterpret_cast<const uint4 *>(&ctl->req[slot])[threadIdx.x];
         __syncthreads();
         const uint32_t op = cur.op;
         if (op == kNskOpQuit) break;
@@ -214,17 +223,23 @@ __global__ void __launch_bounds__(kThreads, 1) kg_nsk(NskRing *ring, NskCtl *ctl
         j.in_place = cur.in_place;
         const uint32_t nr = cur.nr;
         __syncthreads();  // ks ready; cur fully read into registers
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->stamp[slot][2] = globaltimer_ns();  // CTA 0 starts
         if (nr == 10) nsk_run<10>(j, op, sm, ks, lb);
         else if (nr == 12) nsk_run<12>(j, op, sm, ks, lb);
         else nsk_run<14>(j, op, sm, ks, lb);
         __syncthreads();  // this CTA's share is stored
         if (threadIdx.x == 0) {
-            __threadfence_system();
+            if (blockIdx.x == 0) ctl->stamp[slot][3] = globaltimer_ns();  // CTA 0 done
+            // gpu-scope release per CTA; the single system-scope release below
+            // is cumulative over everything that happened-before it.
+            __threadfence();
             const unsigned prev = atomicAdd(&ctl->done_count[slot], 1u);
             if (prev == gridDim.x - 1) {
+                __threadfence();  // acquire side of the counter
+                ctl->stamp[slot][4] = globaltimer_ns();  // last CTA arrived
                 ctl->done_count[slot] = 0;
-                __threadfence_system();
                 st_release_sys_u64(&ring->done[slot], seq);
+                ctl->stamp[slot][5] = globaltimer_ns();  // completion stored
             }
         }
     }

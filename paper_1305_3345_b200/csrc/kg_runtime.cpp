@@ -401,6 +401,19 @@ int nsk_stop_locked() {
     cudaError_t e = cudaStreamSynchronize(g.nsk.st);
     if (e != cudaSuccess) rc = cuda_fail(e, "NSK stop");
     while (g_nsk_waiters.load() != 0) cpu_relax();  // waiters see their done word before the kernel exits
+    if (getenv("KG_NSK_STAMPS")) {
+        static uint64_t st[kg::kNskSlots][8];
+        if (cudaMemcpy(st, g.nsk.ctl->stamp, sizeof st, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            fprintf(stderr, "{\"nsk_stamps_ns\": [");
+            for (int i = 0; i < kg::kNskSlots; i++)
+                fprintf(stderr, "%s[%lld, %lld, %lld, %lld, %lld]", i ? ", " : "",
+                        (long long)(st[i][1] - st[i][0]), (long long)(st[i][2] - st[i][0]),
+                        (long long)(st[i][3] - st[i][0]), (long long)(st[i][4] - st[i][0]),
+                        (long long)(st[i][5] - st[i][0]));
+            fprintf(stderr, "]}\n");
+        }
+        cudaGetLastError();
+    }
     cudaFreeHost(g.nsk.ring);
     cudaFree(g.nsk.ctl);
     cudaStreamDestroy(g.nsk.st);

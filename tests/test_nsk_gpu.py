@@ -1,4 +1,7 @@
 """Row f3: the Non-Stop Kernel (persistent service kernel).
+NB: while the NSK runs, DEVICE-wide synchronisation (torch.cuda.synchronize,
+cudaDeviceSynchronize) waits for the persistent kernel's idle exit, so these
+tests synchronise streams only.
 Parity with the oracle through the NSK in both doorbell modes, device and
 pinned-host buffers, ring wrap-around, idle exit + transparent relaunch,
 stream ordering, stop with outstanding tickets."""
@@ -26,7 +29,7 @@ def run(kg, torch, direction, mode, key, data, n, pb, ivs, where, inplace=False,
     tout = tin if inplace else (torch.empty_like(tin) if where == "device" else torch.empty_like(tin).pin_memory())
     tiv = None if ivs is None else put(torch, ivs, where)
     kg.wait(kg.submit_pages(direction, mode, tin, tout, n, pb, tiv, key_id, stream))
-    torch.cuda.synchronize()
+    (stream or torch.cuda.current_stream()).synchronize()
     return tout.cpu().numpy()
 
 
