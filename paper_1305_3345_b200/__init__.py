@@ -15,7 +15,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkgpu.so")
+LIB_PATH = os.environ.get("KG_LIBKGPU") or os.path.join(_HERE, "libkgpu.so")  # override: experiments only
 
 ENCRYPT, DECRYPT = 0, 1
 MODE_CBC, MODE_ECB = 0, 1

@@ -27,6 +27,7 @@
 //    warp snapshots the one predecessor block it needs from another warp
 //    BEFORE the CTA-wide barrier that precedes the first store.
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "kg_internal.h"
 
@@ -145,22 +146,48 @@ __device__ __forceinline__ uint4 ld_stream(const uint4 *p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(uint4 *p, uint4 v) { __stcs(p, v); }
 
 // 256-bit (two-block) global access: LDG.E.ENL2.256 / STG.E.ENL2.256 on
-// sm_100.  One L1 wavefront moves two blocks of a page chain instead of one.
+// sm_100.  One L1 wavefront moves two blocks.  NOALLOC: L1::no_allocate --
+// measured +3.6% on the per-thread page-chain loads of the CBC-encrypt kernel
+// (profiles/r1m), -1.1% on the warp-coalesced decrypt loads, so the chain
+// kernel uses it and the block-pair kernel does not.  Same for the stores:
+// no_allocate +3.7% on CBC encrypt (568 -> 589 GB/s), -1.1% on decrypt.
+template <bool NOALLOC>
 __device__ __forceinline__ void ld256(const uint4 *p, uint4 &a, uint4 &b) {
-    asm volatile("ld.global.cs.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                 : "l"(p));
+    if (NOALLOC)
+        asm volatile("ld.global.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                     : "l"(p));
+    else
+        asm volatile("ld.global.cs.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                     : "l"(p));
 }
+template <bool NOALLOC>
 __device__ __forceinline__ void st256(uint4 *p, uint4 a, uint4 b) {
-    asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
-                 "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-                 : "memory");
+    if (NOALLOC)
+        asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
+                     "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                     : "memory");
+    else
+        asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+                     "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                     : "memory");
 }
 
 // Balanced split of [0, n) into g parts: start of part k.
 __device__ __forceinline__ uint64_t part_start(uint64_t n, uint64_t g, uint64_t k) {
     const uint64_t q = n / g, r = n % g;
     return k * q + (k < r ? k : r);
+}
+
+// Programmatic dependent launch (sm_90+): the table fill above does not touch
+// the batch, so it may overlap the tail of the previous kernel on the stream;
+// griddepcontrol.wait then blocks until that kernel has completed and its
+// memory is visible.  launch_dependents lets the next launch on the stream
+// start its own prologue on SMs this grid has already vacated.
+__device__ __forceinline__ void pdl_prologue_done() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 __device__ __forceinline__ uint32_t lane_bytes() {
@@ -267,6 +294,70 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
     }
 }
 
+// ---- block-pair body (m even): each lane owns two consecutive blocks --------
+// Same contract as blockpar_body, but a warp unit is 64 blocks (1 KiB) moved
+// with one LDG.256/STG.256 per lane; the CBC predecessor of the lane's first
+// block is the previous lane's second block (one 4-word SHFL per 64 blocks),
+// that of its second block is its own first block.  A pair never straddles a
+// page (m even, ranges in whole pairs).
+template <bool DEC, bool CBC, class Cipher>
+__device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint64_t mp = a.m >> 1;  // pairs per page
+    uint64_t c0, c1;               // CTA range in pairs
+    if (a.in_place) {
+        c0 = part_start(a.n_pages, ncta, cta) * mp;
+        c1 = part_start(a.n_pages, ncta, cta + 1) * mp;
+    } else {
+        const uint64_t np = a.n_pages * mp;
+        c0 = part_start(np, ncta, cta);
+        c1 = part_start(np, ncta, cta + 1);
+    }
+    const uint64_t w0 = c0 + part_start(c1 - c0, nwarps, warp);
+    const uint64_t w1 = c0 + part_start(c1 - c0, nwarps, warp + 1);
+    uint64_t page = (w0 + lane) / mp;
+    uint32_t jp = (uint32_t)((w0 + lane) - page * mp);  // pair index in the page
+
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    if (CBC && DEC) {
+        if (w0 < w1 && (w0 % mp) != 0) carry = a.in[2 * w0 - 1];
+    }
+    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+    if (w0 + lane < w1) ld256<false>(a.in + 2 * (w0 + lane), n0, n1);
+    __syncthreads();
+
+    for (uint64_t u = w0; u < w1; u += 32) {
+        const uint64_t q = u + lane;
+        const bool act = q < w1;
+        const uint4 x0 = n0, x1 = n1;
+        if (q + 32 < w1) ld256<false>(a.in + 2 * (q + 32), n0, n1);
+        uint4 prev = make_uint4(0, 0, 0, 0);
+        if (CBC && DEC) {
+            const uint4 r = shfl4(x1, (lane + 31) & 31);
+            prev = (lane == 0) ? carry : r;
+            carry = r;
+            if (act && jp == 0) prev = a.ivs[page];
+        }
+        uint4 o0 = cph.rounds(cph.first(x0));
+        uint4 o1 = cph.rounds(cph.first(x1));
+        if (CBC && DEC) {
+            o0 = xor4(o0, prev);
+            o1 = xor4(o1, x0);
+        }
+        if (act) st256<false>(a.out + 2 * q, o0, o1);
+        jp += 32;
+        if (jp >= mp) {
+            if (mp >= 32) {
+                jp -= (uint32_t)mp;
+                ++page;
+            } else {
+                page += jp / (uint32_t)mp;
+                jp %= (uint32_t)mp;
+            }
+        }
+    }
+}
+
 // ---- chain body: CBC encrypt, one thread per page chain ------------------------
 // WIDE (m even): blocks move two at a time with 256-bit loads/stores.
 template <bool WIDE, class Cipher>
@@ -280,14 +371,14 @@ __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, ui
         uint4 prev = a.ivs[p];  // C_{p,-1} := IV_p
         if (WIDE) {
             uint4 x0, x1;
-            ld256(src, x0, x1);
+            ld256<true>(src, x0, x1);
             for (uint32_t j = 0; j < m; j += 2) {
                 uint4 n0 = x0, n1 = x1;
-                if (j + 2 < m) ld256(src + j + 2, n0, n1);  // prefetch P_{j+2}, P_{j+3}
+                if (j + 2 < m) ld256<true>(src + j + 2, n0, n1);  // prefetch P_{j+2}, P_{j+3}
                 // C_j = E_K(P_j ^ C_{j-1}); the first AddRoundKey folds into the same XOR
                 const uint4 c0 = cph.rounds(cph.first(xor4(x0, prev)));
                 prev = cph.rounds(cph.first(xor4(x1, c0)));
-                st256(dst + j, c0, prev);
+                st256<true>(dst + j, c0, prev);
                 x0 = n0;
                 x1 = n1;
             }
@@ -316,21 +407,28 @@ __device__ __forceinline__ Job job_of(const LaunchArgs &a) {
 }
 
 // ---- launch-per-batch kernels -------------------------------------------------
-template <int NR, int DIR, int MODE>
+template <int NR, int DIR, int MODE, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
     constexpr bool DEC = (DIR == 1);
     constexpr bool CBC = (MODE == 0);
     fill_tables<DEC>(sm);
+    pdl_prologue_done();
     const uint32_t lb = lane_bytes();
-    if (DEC) blockpar_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
-    else blockpar_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+    if (PAIR) {
+        if (DEC) blockpair_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+        else blockpair_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+    } else {
+        if (DEC) blockpar_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+        else blockpar_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+    }
 }
 
 template <int NR, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
     fill_tables<false>(sm);
+    pdl_prologue_done();
     __syncthreads();
     cbc_enc_body<WIDE>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
 }
@@ -345,12 +443,35 @@ cudaError_t set_smem(K kernel, int bytes) {
 template <int NR>
 cudaError_t init_nr() {
     cudaError_t e;
-    if ((e = set_smem(kg_blockpar<NR, 1, 0>, kSmemDec)) != cudaSuccess) return e;
-    if ((e = set_smem(kg_blockpar<NR, 1, 1>, kSmemDec)) != cudaSuccess) return e;
-    if ((e = set_smem(kg_blockpar<NR, 0, 1>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 0, false>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 1, false>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 0, 1, false>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 0, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 1, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 0, 1, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, false>, kSmemEnc)) != cudaSuccess) return e;
     return cudaSuccess;
+}
+
+// Launch with the programmatic-stream-serialization attribute (PDL).
+template <typename... KArgs>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaStream_t st, const LaunchArgs &a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    static const int use_pdl = [] {
+        const char *e = getenv("KG_PDL");
+        return (e && *e == '0') ? 0 : 1;
+    }();
+    cfg.numAttrs = use_pdl;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
 template <int NR>
@@ -358,19 +479,26 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     if (dir == 0 && mode == 0) {
         const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
-        if ((a.m & 1) == 0) kg_cbc_enc<NR, true><<<grid, kThreads, kSmemEnc, st>>>(a);
-        else kg_cbc_enc<NR, false><<<grid, kThreads, kSmemEnc, st>>>(a);
-        return cudaGetLastError();
+        if ((a.m & 1) == 0) return launch_pdl(kg_cbc_enc<NR, true>, grid, kSmemEnc, st, a);
+        return launch_pdl(kg_cbc_enc<NR, false>, grid, kSmemEnc, st, a);
     }
     uint64_t want = (nb + 255) / 256;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
     if (want < 1) want = 1;
     const unsigned grid = (unsigned)want;
-    if (dir == 1 && mode == 0) kg_blockpar<NR, 1, 0><<<grid, kThreads, kSmemDec, st>>>(a);
-    else if (dir == 1) kg_blockpar<NR, 1, 1><<<grid, kThreads, kSmemDec, st>>>(a);
-    else kg_blockpar<NR, 0, 1><<<grid, kThreads, kSmemEnc, st>>>(a);
-    return cudaGetLastError();
+    static const int pair_ok = [] {
+        const char *e = getenv("KG_PAIR");
+        return (e && *e == '0') ? 0 : 1;
+    }();
+    if (pair_ok && (a.m & 1) == 0) {
+        if (dir == 1 && mode == 0) return launch_pdl(kg_blockpar<NR, 1, 0, true>, grid, kSmemDec, st, a);
+        if (dir == 1) return launch_pdl(kg_blockpar<NR, 1, 1, true>, grid, kSmemDec, st, a);
+        return launch_pdl(kg_blockpar<NR, 0, 1, true>, grid, kSmemEnc, st, a);
+    }
+    if (dir == 1 && mode == 0) return launch_pdl(kg_blockpar<NR, 1, 0, false>, grid, kSmemDec, st, a);
+    if (dir == 1) return launch_pdl(kg_blockpar<NR, 1, 1, false>, grid, kSmemDec, st, a);
+    return launch_pdl(kg_blockpar<NR, 0, 1, false>, grid, kSmemEnc, st, a);
 }
 
 }  // namespace
