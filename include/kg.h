@@ -147,11 +147,13 @@ KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);
 
 /* How batches touching pinned host memory reach the GPU (rows a3/a8 vs f4):
  *   KG_HOST_STAGED   copy engines move chunks through the device staging ring
- *                    (H2D || kernel || D2H on three streams; default);
+ *                    (H2D || kernel || D2H on three streams);
  *   KG_HOST_ZEROCOPY the kernel reads and writes the caller's pinned pages
  *                    directly over the host link (no copies, one launch) --
  *                    the paper's §4 "save an extra copy" idea;
- *   KG_HOST_AUTO     zero-copy for batches of at most zc_max_bytes, staged above.
+ *   KG_HOST_AUTO     zero-copy for batches of at most zc_max_bytes, staged above;
+ *                    CBC encryption (serial per-page chains, 32-byte accesses)
+ *                    is always staged.  Default: AUTO with zc_max_bytes = 32 MiB.
  * Takes effect for later submits.  Environment override at kg_init:
  * KG_HOST_PATH=0|1|2.  Errors: KG_ENOTINIT, KG_EINVAL (bad mode). */
 #define KG_HOST_STAGED 0
@@ -183,6 +185,19 @@ KG_API int kg_set_host_path(int mode, uint64_t zc_max_bytes);
 #define KG_NSK_DIRECT 1
 KG_API int kg_nsk_start(int ctas, int flags, uint32_t idle_ms);
 KG_API int kg_nsk_stop(void);
+
+/* Size-based dispatch while the NSK runs (row f2; the paper's "calibrating
+ * the crossover point at boot", between its two GPU paths):
+ * requests of at most max_bytes (n_pages*page_bytes) go to the NSK, larger
+ * ones are launched as ordinary kernels on the SMs the NSK leaves free (the
+ * paper's "switches to a traditional CUDA kernel launch").
+ * max_bytes = 0 calibrates: times both paths on 1..8192-page AES-128 decrypt
+ * batches in device memory and keeps the largest size where the NSK is not
+ * slower (a tie goes to the NSK).  UINT64_MAX = everything to the NSK (the
+ * default after kg_nsk_start).  *chosen (may be NULL) receives the threshold.
+ * There is no CPU leg: the library has no CPU path by design.
+ * Errors: KG_ENOTINIT, KG_EINVAL (NSK not running), KG_ENOMEM, KG_ECUDA. */
+KG_API int kg_nsk_dispatch(uint64_t max_bytes, uint64_t *chosen);
 
 /* Number of CUDA kernels this library has launched in this process
  * (instrumentation for benchmarks; monotonic, never reset). */

@@ -26,7 +26,7 @@ MAX_INFLIGHT = 65536
 #: every symbol include/kg.h declares
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
                "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path",
-               "kg_nsk_start", "kg_nsk_stop")
+               "kg_nsk_start", "kg_nsk_stop", "kg_nsk_dispatch")
 NSK_DIRECT = 1
 HOST_STAGED, HOST_ZEROCOPY, HOST_AUTO = 0, 1, 2
 
@@ -58,6 +58,8 @@ _lib.kg_nsk_start.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint32]
 _lib.kg_nsk_start.restype = ctypes.c_int
 _lib.kg_nsk_stop.argtypes = []
 _lib.kg_nsk_stop.restype = ctypes.c_int
+_lib.kg_nsk_dispatch.argtypes = [ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+_lib.kg_nsk_dispatch.restype = ctypes.c_int
 _lib.kg_launch_count.argtypes = []
 _lib.kg_launch_count.restype = ctypes.c_uint64
 
@@ -158,6 +160,14 @@ def nsk_start(ctas: int = 0, flags: int = 0, idle_ms: int = 0) -> None:
 
 def nsk_stop() -> None:
     _check(_lib.kg_nsk_stop(), "kg_nsk_stop")
+
+
+def nsk_dispatch(max_bytes: int = 0) -> int:
+    """Route requests <= max_bytes to the NSK, larger ones to launches (0 = calibrate).
+    Returns the threshold in use."""
+    out = ctypes.c_uint64(0)
+    _check(_lib.kg_nsk_dispatch(int(max_bytes), ctypes.byref(out)), "kg_nsk_dispatch")
+    return int(out.value)
 
 
 def launch_count() -> int:

@@ -24,6 +24,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <time.h>
+
 #include <atomic>
 #include <mutex>
 #include <unordered_map>
@@ -60,6 +62,8 @@ struct Nsk {
     cudaStream_t st = nullptr;
     uint64_t seq = 0;            // last sequence number handed out
     uint64_t gen = 0;            // incremented at every stop
+    uint64_t dispatch_bytes = UINT64_MAX;  // requests up to this size go to the NSK (row f2)
+    uint8_t *cal_in = nullptr, *cal_out = nullptr, *cal_iv = nullptr;  // calibration scratch
 };
 
 typedef CUresult (*PFN_writeValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
@@ -88,8 +92,8 @@ struct Ctx {
     int n_slots = 3;
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
-    int host_path = KG_HOST_STAGED;
-    uint64_t zc_max_bytes = 1ull << 20;
+    int host_path = KG_HOST_AUTO;
+    uint64_t zc_max_bytes = 32ull << 20;  // zero-copy beats staging up to 32 MiB (tools/sweep.py, r1p)
     Nsk nsk;
     PFN_writeValue64 write_value64 = nullptr;
     PFN_waitValue64 wait_value64 = nullptr;
@@ -249,7 +253,9 @@ int64_t new_ticket(cudaStream_t st) {
 }
 
 int launch(int dir, int mode, int nr, const kg::LaunchArgs &a, cudaStream_t st) {
-    cudaError_t e = kg::launch_pages(dir, mode, nr, a, g.num_sms, st);
+    // While the NSK holds some SMs, launched kernels use the others.
+    const int sms = g.nsk.on ? g.num_sms - g.nsk.ctas : g.num_sms;
+    cudaError_t e = kg::launch_pages(dir, mode, nr, a, sms > 0 ? sms : 1, st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_pages");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return KG_OK;
@@ -416,6 +422,9 @@ int nsk_stop_locked() {
     }
     cudaFreeHost(g.nsk.ring);
     cudaFree(g.nsk.ctl);
+    cudaFree(g.nsk.cal_in);
+    cudaFree(g.nsk.cal_out);
+    cudaFree(g.nsk.cal_iv);
     cudaStreamDestroy(g.nsk.st);
     const uint64_t gen = g.nsk.gen + 1;
     g.nsk = Nsk();
@@ -562,8 +571,9 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const kg::RoundKeys &rk = (dir == KG_ENCRYPT) ? ks.enc : ks.dec;  // snapshot: copied into LaunchArgs
     int rc;
-    if (g.nsk.on) {
-        // Every request goes to the resident service kernel (it owns its SMs).
+    if (g.nsk.on && total <= g.nsk.dispatch_bytes) {
+        // Small requests go to the resident service kernel as messages; larger
+        // ones (row f2 dispatch) are launched on the SMs the NSK leaves free.
         if (!zin || !zout || (need_iv && !ziv)) return KG_EINVAL;
         const uint32_t op = (uint32_t)dir | ((uint32_t)mode << 1);
         const int64_t seq = nsk_post(op, zin, const_cast<void *>(zout), need_iv ? ziv : nullptr, n_pages,
@@ -579,9 +589,12 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
     const bool all_device = (kin == K_DEVICE && kout == K_DEVICE && kiv == K_DEVICE);
     // Zero-copy (row f4): the kernel reads and writes the
     // caller's pinned pages over the host link, no staging copies.
+    // AUTO never zero-copies CBC encryption: its per-thread page chains read
+    // 32 B at a time, which the host link serves at ~5 GB/s (profiles/r1_pinned).
+    const bool chain = (dir == KG_ENCRYPT && mode == KG_MODE_CBC);
     const bool zero_copy = !all_device && zin && zout && (!need_iv || ziv) &&
                            (g.host_path == KG_HOST_ZEROCOPY ||
-                            (g.host_path == KG_HOST_AUTO && total <= g.zc_max_bytes));
+                            (g.host_path == KG_HOST_AUTO && !chain && total <= g.zc_max_bytes));
     if (all_device || zero_copy) {
         kg::LaunchArgs a;
         a.in = reinterpret_cast<const uint4 *>(zin);
@@ -714,6 +727,89 @@ int kg_nsk_start(int ctas, int flags, uint32_t idle_ms) {
         g.nsk.gen = gen;
     }
     return rc;
+}
+
+// Row f2: size-based dispatch between the NSK (message to a resident kernel)
+// and launch-per-batch, calibrated on the device (the paper calibrates a
+// CPU/GPU crossover at boot; here both legs are GPU paths:
+// the library has no CPU path by design).  Caller holds g_mu.
+static double now_s() {
+    timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return t.tv_sec + 1e-9 * t.tv_nsec;
+}
+
+int nsk_calibrate(uint64_t *chosen) {
+    const uint32_t pb = 4096;
+    const uint64_t max_pages = 1u << 13;  // up to 32 MiB
+    // Scratch lives until kg_nsk_stop: cudaFree would synchronise the whole
+    // device, i.e. wait for the resident kernel's idle exit.
+    if (!g.nsk.cal_in) {
+        if (cudaMalloc(&g.nsk.cal_in, max_pages * pb) != cudaSuccess ||
+            cudaMalloc(&g.nsk.cal_out, max_pages * pb) != cudaSuccess ||
+            cudaMalloc(&g.nsk.cal_iv, max_pages * 16) != cudaSuccess) {
+            cudaGetLastError();
+            return KG_ENOMEM;
+        }
+    }
+    uint8_t *d_in = g.nsk.cal_in, *d_out = g.nsk.cal_out, *d_iv = g.nsk.cal_iv;
+    uint8_t key[16];
+    for (int i = 0; i < 16; i++) key[i] = (uint8_t)(17 * i + 1);
+    kg::RoundKeys enc, dec;
+    const int nr = kg::expand_key(key, 16, &enc, &dec);
+    cudaStream_t st;
+    KG_CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaMemsetAsync(d_in, 0x5a, max_pages * pb, st);
+    cudaMemsetAsync(d_iv, 0x33, max_pages * 16, st);
+    cudaStreamSynchronize(st);
+    uint64_t best = 0;
+    int rc = KG_OK;
+    for (uint64_t pages = 1; pages <= max_pages && rc == KG_OK; pages *= 4) {
+        double t_nsk = 1e9, t_launch = 1e9;
+        for (int rep = 0; rep < 7; rep++) {
+            double t0 = now_s();
+            const int64_t seq = nsk_post(1, d_in, d_out, d_iv, pages, pb / 16, 0, nr, &dec, st, true);
+            if (seq < 0) {
+                rc = (int)seq;
+                break;
+            }
+            const uint64_t *done = &g.nsk.ring->done[(seq - 1) % kg::kNskSlots];
+            while (vload(done) < (uint64_t)seq) cpu_relax();
+            double t1 = now_s();
+            kg::LaunchArgs a;
+            a.in = reinterpret_cast<const uint4 *>(d_in);
+            a.out = reinterpret_cast<uint4 *>(d_out);
+            a.ivs = reinterpret_cast<const uint4 *>(d_iv);
+            a.n_pages = pages;
+            a.m = pb / 16;
+            a.in_place = 0;
+            a.rk = dec;
+            rc = launch(1, 0, nr, a, st);
+            if (rc != KG_OK) break;
+            cudaStreamSynchronize(st);
+            double t2 = now_s();
+            if (rep >= 2) {  // first reps warm up
+                t_nsk = (t1 - t0) < t_nsk ? (t1 - t0) : t_nsk;
+                t_launch = (t2 - t1) < t_launch ? (t2 - t1) : t_launch;
+            }
+        }
+        if (t_nsk <= t_launch) best = pages * pb;  // a tie goes to the resident kernel
+    }
+    cudaStreamDestroy(st);
+    if (rc != KG_OK) return rc;
+    g.nsk.dispatch_bytes = best;
+    if (chosen) *chosen = best;
+    return KG_OK;
+}
+
+int kg_nsk_dispatch(uint64_t max_bytes, uint64_t *chosen) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.up) return KG_ENOTINIT;
+    if (!g.nsk.on) return KG_EINVAL;
+    if (max_bytes == 0) return nsk_calibrate(chosen);
+    g.nsk.dispatch_bytes = max_bytes;
+    if (chosen) *chosen = max_bytes;
+    return KG_OK;
 }
 
 int kg_nsk_stop(void) {

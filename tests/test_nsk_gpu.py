@@ -137,3 +137,28 @@ def test_nsk_stop_with_outstanding_and_restart(nsk):
     regular = torch.empty_like(x)
     kg.wait(kg.submit_pages(0, 0, x, regular, n, pb, iv, 0))   # launch-per-batch path again
     assert torch.equal(ref, regular) and torch.equal(y, regular)
+
+
+def test_nsk_size_dispatch(nsk):
+    """Row f2: small requests to the NSK, large ones launched on the free SMs."""
+    kg, torch = nsk
+    kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+    thr = kg.nsk_dispatch(0)                 # calibrate
+    assert thr % 4096 == 0
+    kg.nsk_dispatch(64 << 10)                # force: <= 16 pages to the NSK
+    key = synth.make_key(16, seed=40)
+    for n in (4, 16, 17, 3000):
+        data = synth.make_pages(n, 4096, seed=n)
+        ivs = synth.make_ivs(n, seed=n + 1)
+        exp = oracle_pages(1, 0, key, data, n, 4096, ivs)
+        l0 = kg.launch_count()
+        got = run(kg, torch, 1, 0, key, data, n, 4096, ivs, "device")
+        launched = kg.launch_count() - l0
+        assert first_mismatch(got, exp) is None, n
+        assert launched == (0 if n <= 16 else 1), (n, launched)
+    # pinned + large goes through the staged path on the remaining SMs
+    n = 5000
+    data = synth.make_pages(n, 4096, seed=77)
+    ivs = synth.make_ivs(n, seed=78)
+    exp = oracle_pages(0, 0, key, data, n, 4096, ivs)
+    assert first_mismatch(run(kg, torch, 0, 0, key, data, n, 4096, ivs, "pinned"), exp) is None

@@ -38,10 +38,19 @@ def test_cbc_device_in_place(direction, n, pb):
     assert first_mismatch(got, exp) is None
 
 
+@pytest.fixture(params=["staged", "auto"])
+def host_path(request):
+    from gpu_util import kg_ready
+    kg, _ = kg_ready()
+    kg.set_host_path(kg.HOST_STAGED if request.param == "staged" else kg.HOST_AUTO, 32 << 20)
+    yield request.param
+    kg.set_host_path(kg.HOST_AUTO, 32 << 20)
+
+
 @pytest.mark.parametrize("n,pb", [(1, 16), (16, 4096), (149, 4096), (1000, 512), (3000, 4096)])
 @pytest.mark.parametrize("direction", [0, 1])
 @pytest.mark.parametrize("inplace", [False, True])
-def test_cbc_pinned(direction, n, pb, inplace):
+def test_cbc_pinned(direction, n, pb, inplace, host_path):
     key = synth.make_key(32, seed=7 * n + pb)
     data = synth.make_pages(n, pb, seed=n)
     ivs = synth.make_ivs(n, seed=n + 9)
@@ -53,7 +62,7 @@ def test_cbc_pinned(direction, n, pb, inplace):
 @pytest.mark.parametrize("in_where,out_where,iv_where", [("device", "pinned", "device"), ("pinned", "device", "pinned"),
                                                          ("pinned", "pinned", "device"), ("device", "device", "pinned")])
 @pytest.mark.parametrize("direction", [0, 1])
-def test_cbc_mixed_residency(direction, in_where, out_where, iv_where):
+def test_cbc_mixed_residency(direction, in_where, out_where, iv_where, host_path):
     n, pb = 700, 4096
     key = synth.make_key(16, seed=77)
     data = synth.make_pages(n, pb, seed=78)
@@ -86,12 +95,14 @@ def test_small_staging_chunks_many_slots():
     data = synth.make_pages(n, pb, seed=6)
     ivs = synth.make_ivs(n, seed=7)
     exp = oracle_pages(1, 0, key, data, n, pb, ivs)
+    kg.set_host_path(kg.HOST_STAGED)
     for chunk, slots in [(4096, 2), (3 * 4096, 3), (64 * 1024, 8), (10 * 4096 + 16, 3)]:
         kg.set_pipeline(chunk, slots)
         try:
             got = gpu_pages(1, 0, key, data, n, pb, ivs, where="pinned")
         finally:
             kg.set_pipeline(16 << 20, 3)
+            kg.set_host_path(kg.HOST_AUTO, 32 << 20)
         assert first_mismatch(got, exp) is None, (chunk, slots)
 
 
@@ -112,7 +123,7 @@ def test_cbc_host_zero_copy(direction, n, pb, mode):
         got_ip = gpu_pages(direction, 0, key, data, n, pb, ivs, where="pinned", inplace=True)
         got_mixed = gpu_pages(direction, 0, key, data, n, pb, ivs, where="pinned", out_where="device")
     finally:
-        kg.set_host_path(kg.HOST_STAGED)
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)
     assert first_mismatch(got, exp) is None
     assert first_mismatch(got_ip, exp) is None
     assert first_mismatch(got_mixed, exp) is None

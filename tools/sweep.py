@@ -73,10 +73,27 @@ def main():
             for _ in range(3):
                 f()
         th = lat(run_hbm, reps)
+        kg.set_host_path(kg.HOST_STAGED)
         tp = lat(run_pin, reps)
+        kg.set_host_path(kg.HOST_ZEROCOPY)
+        tz = lat(run_pin, reps)
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)
+        tn = tnp = None
+        if n <= 4096:  # the NSK (row f3), direct doorbell, 16 SMs
+            kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+            for _ in range(5):
+                run_hbm()
+            tn = lat(run_hbm, reps)
+            tnp = lat(run_pin, reps)
+            kg.nsk_stop()
         row = {"pages": n, "bytes": n * PB,
                "hbm_us_p10": 1e6 * pct(th, 10), "hbm_us_p50": 1e6 * pct(th, 50), "hbm_us_p90": 1e6 * pct(th, 90),
                "pinned_us_p10": 1e6 * pct(tp, 10), "pinned_us_p50": 1e6 * pct(tp, 50), "pinned_us_p90": 1e6 * pct(tp, 90)}
+        row["zerocopy_us_p50"] = 1e6 * pct(tz, 50)
+        if tn:
+            row["nsk_hbm_us_p50"] = 1e6 * pct(tn, 50)
+            row["nsk_pinned_us_p50"] = 1e6 * pct(tnp, 50)
+        row["zerocopy_gbs"] = n * PB / (row["zerocopy_us_p50"] * 1e-6) / 1e9
         row["hbm_gbs"] = n * PB / (row["hbm_us_p50"] * 1e-6) / 1e9
         row["pinned_gbs"] = n * PB / (row["pinned_us_p50"] * 1e-6) / 1e9
         if k <= a.oracle_kmax:
@@ -89,17 +106,34 @@ def main():
             row["oracle_1t_us_p50"] = 1e6 * pct(t1, 50)
             row["oracle_all_us_p50"] = 1e6 * pct(tt, 50)
             row["oracle_best_us"] = min(row["oracle_1t_us_p50"], row["oracle_all_us_p50"])
+        # context line, NOT the oracle: single-core OpenSSL (AES-NI) CBC, like the
+        # paper's SSE-optimised in-kernel AES comparator
+        try:
+            from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
+            cb = data[: n * PB].numpy().tobytes()
+            ivb = ivs[: 16 * n].numpy().tobytes()
+
+            def ossl():
+                for p in range(n):
+                    d = Cipher(algorithms.AES(key), modes.CBC(ivb[16 * p:16 * p + 16])).decryptor()
+                    d.update(cb[p * PB:(p + 1) * PB])
+
+            to = lat(ossl, 20 if k < 8 else 3)
+            row["openssl_aesni_1core_us_p50"] = 1e6 * pct(to, 50)
+        except Exception:  # noqa: BLE001
+            pass
         rows.append(row)
         lines.append(json.dumps(row))
         print(lines[-1], flush=True)
     summ = {"summary": "c4_sweep", "oracle_threads": threads}
-    for res in ("hbm", "pinned"):
-        cross = None
-        for r in rows:
-            if "oracle_best_us" in r and r[f"{res}_us_p50"] <= r["oracle_best_us"]:
-                cross = r["bytes"]
-                break
-        summ[f"crossover_bytes_{res}"] = cross
+    for res in ("hbm", "pinned", "zerocopy", "nsk_hbm", "nsk_pinned"):
+        for ref, key_ in (("oracle", "oracle_best_us"), ("openssl_aesni_1core", "openssl_aesni_1core_us_p50")):
+            cross = None
+            for r in rows:
+                if key_ in r and f"{res}_us_p50" in r and r[f"{res}_us_p50"] <= r[key_]:
+                    cross = r["bytes"]
+                    break
+            summ[f"crossover_bytes_{res}_vs_{ref}"] = cross
     print(json.dumps(summ), flush=True)
     if a.out:
         with open(a.out, "w") as f:
