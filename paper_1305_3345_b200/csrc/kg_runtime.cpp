@@ -76,6 +76,7 @@ struct Slot {
 };
 
 constexpr int kMaxSlots = 8;
+constexpr uint64_t kIvStageMax = 256ull << 20;  // IVs of up to 16M pages (64 GiB of 4 KiB pages)
 
 struct Ctx {
     bool up = false;
@@ -92,6 +93,8 @@ struct Ctx {
     int n_slots = 3;
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
+    uint8_t *iv_stage = nullptr;  // batch IVs of host batches (<= kIvStageMax)
+    uint64_t iv_stage_bytes = 0;
     int host_path = KG_HOST_AUTO;
     uint64_t zc_max_bytes = 32ull << 20;  // zero-copy beats staging up to 32 MiB (tools/sweep.py, r1p)
     Nsk nsk;
@@ -262,6 +265,26 @@ int launch(int dir, int mode, int nr, const kg::LaunchArgs &a, cudaStream_t st) 
 }
 
 // Host-memory batch: chunked H2D -> compute -> D2H through the staging ring.
+// Host IVs move in ONE copy ahead of the first chunk into a batch-sized IV
+// buffer.  A small per-chunk IV copy gets queued by the copy engines behind
+// the previous chunk's D2H, which delayed every kernel by a whole D2H; reading
+// them in place over the host link slowed the kernels instead
+// (profiles/r1_pinned: trace_*).
+int ensure_iv_stage(uint64_t bytes) {
+    if (g.iv_stage_bytes >= bytes) return KG_OK;
+    cudaStreamSynchronize(g.s_h2d);
+    cudaStreamSynchronize(g.s_comp);
+    if (g.iv_stage) cudaFree(g.iv_stage);
+    g.iv_stage = nullptr;
+    g.iv_stage_bytes = 0;
+    if (cudaMalloc(&g.iv_stage, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return KG_ENOMEM;
+    }
+    g.iv_stage_bytes = bytes;
+    return KG_OK;
+}
+
 int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint8_t *in, Kind kin,
                   uint8_t *out, Kind kout, uint64_t n_pages, uint32_t page_bytes, const uint8_t *ivs,
                   Kind kiv, cudaStream_t st) {
@@ -277,16 +300,39 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     KG_CU(cudaStreamWaitEvent(g.s_h2d, g.ev_begin, 0));
     KG_CU(cudaStreamWaitEvent(g.s_comp, g.ev_begin, 0));
     KG_CU(cudaStreamWaitEvent(g.s_d2h, g.ev_begin, 0));
+    // all host IVs in one copy (if they fit the cap), ahead of chunk 0's pages
+    const bool iv_upfront = need_iv && kiv == K_HOST && 16 * n_pages <= kIvStageMax &&
+                            ensure_iv_stage(16 * n_pages) == KG_OK;
+    if (iv_upfront) KG_CU(cudaMemcpyAsync(g.iv_stage, ivs, 16 * n_pages, cudaMemcpyHostToDevice, g.s_h2d));
 
-    uint64_t i = 0;
-    for (uint64_t p0 = 0; p0 < n_pages; p0 += chunk_pages, ++i) {
-        const uint64_t np = (n_pages - p0 < chunk_pages) ? (n_pages - p0) : chunk_pages;
+    // Chunk schedule.  The first H2D and the last D2H overlap nothing, so for
+    // batches of >= 4 chunks the ends ramp C/8, C/4, C/2 (... C ...) C/2, C/4,
+    // C/8: fill and drain shrink 8x for a few extra chunks (profiles/r1_pinned).
+    std::vector<uint64_t> sched;
+    {
+        uint64_t left = n_pages;
+        std::vector<uint64_t> ramp;
+        if (n_pages >= 4 * chunk_pages && chunk_pages >= 8)
+            for (uint64_t d = 8; d >= 2; d /= 2) ramp.push_back(chunk_pages / d);
+        for (uint64_t r : ramp) sched.push_back(r), left -= 2 * r;
+        std::vector<uint64_t> mid;
+        while (left > 0) {
+            const uint64_t np = left < chunk_pages ? left : chunk_pages;
+            mid.push_back(np);
+            left -= np;
+        }
+        sched.insert(sched.end(), mid.begin(), mid.end());
+        for (size_t r = ramp.size(); r-- > 0;) sched.push_back(ramp[r]);
+    }
+    uint64_t p0 = 0;
+    for (uint64_t i = 0; i < sched.size(); p0 += sched[i], ++i) {
+        const uint64_t np = sched[i];
         const uint64_t off = p0 * page_bytes, nbytes = np * page_bytes;
         Slot &s = g.slots[i % (uint64_t)g.n_slots];
         // H2D stage: wait until the slot's previous output has drained.
         KG_CU(cudaStreamWaitEvent(g.s_h2d, s.freed, 0));
         if (kin == K_HOST) KG_CU(cudaMemcpyAsync(s.data, in + off, nbytes, cudaMemcpyHostToDevice, g.s_h2d));
-        if (need_iv && kiv == K_HOST)
+        if (need_iv && kiv == K_HOST && !iv_upfront)
             KG_CU(cudaMemcpyAsync(s.ivs, ivs + 16 * p0, 16 * np, cudaMemcpyHostToDevice, g.s_h2d));
         KG_CU(cudaEventRecord(s.loaded, g.s_h2d));
         trace(i, 'h', g.s_h2d);
@@ -295,7 +341,9 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         kg::LaunchArgs a;
         a.in = reinterpret_cast<const uint4 *>(kin == K_HOST ? s.data : in + off);
         a.out = reinterpret_cast<uint4 *>(kout == K_HOST ? s.data : out + off);
-        a.ivs = need_iv ? reinterpret_cast<const uint4 *>(kiv == K_HOST ? s.ivs : ivs + 16 * p0) : nullptr;
+        a.ivs = !need_iv ? nullptr
+                : reinterpret_cast<const uint4 *>(kiv != K_HOST ? ivs + 16 * p0
+                                                  : iv_upfront ? g.iv_stage + 16 * p0 : s.ivs);
         a.n_pages = np;
         a.m = page_bytes / 16;
         a.in_place = (const void *)a.in == (const void *)a.out;
@@ -829,6 +877,9 @@ int kg_shutdown(void) {
     for (cudaEvent_t e : g.ev_pool) cudaEventDestroy(e);
     g.ev_pool.clear();
     free_staging();
+    if (g.iv_stage) cudaFree(g.iv_stage);
+    g.iv_stage = nullptr;
+    g.iv_stage_bytes = 0;
     for (int i = 0; i < kMaxSlots; i++) {
         cudaEventDestroy(g.slots[i].loaded);
         cudaEventDestroy(g.slots[i].done);

@@ -8,6 +8,10 @@
 
 #include <vector>
 
+__global__ void noop_kernel(uint4 *p, size_t n) {
+    if (n == 0xFFFFFFFFFFFull) p[threadIdx.x] = make_uint4(0, 0, 0, 0);
+}
+
 __global__ void touch(uint4 *p, size_t n) {
     size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     for (; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -17,6 +21,7 @@ __global__ void touch(uint4 *p, size_t n) {
     }
 }
 
+static int g_kernel_kind = 0;  // 0 touch<<<148,1024>>>, 1 noop<<<148,1024,smem>>>, 2 noop<<<1,32>>>
 static float run(const char *name, uint8_t *hin, uint8_t *hout, uint8_t **stage, int slots, size_t total, size_t chunk,
                  bool with_kernel, bool events, cudaStream_t sh, cudaStream_t sk, cudaStream_t sd, int smem) {
     std::vector<cudaEvent_t> loaded(slots), done(slots), freed(slots);
@@ -43,7 +48,9 @@ static float run(const char *name, uint8_t *hin, uint8_t *hout, uint8_t **stage,
             if (events) cudaEventRecord(loaded[s], sh);
             if (with_kernel) {
                 if (events) cudaStreamWaitEvent(sk, loaded[s], 0);
-                touch<<<148, 1024, smem, sk>>>((uint4 *)stage[s], nb / 16);
+                if (g_kernel_kind == 0) touch<<<148, 1024, smem, sk>>>((uint4 *)stage[s], nb / 16);
+                else if (g_kernel_kind == 1) noop_kernel<<<148, 1024, smem, sk>>>((uint4 *)stage[s], nb / 16);
+                else noop_kernel<<<1, 32, 0, sk>>>((uint4 *)stage[s], nb / 16);
                 if (events) cudaEventRecord(done[s], sk);
                 if (events) cudaStreamWaitEvent(sd, done[s], 0);
             } else if (events) {
@@ -153,6 +160,18 @@ int main() {
         zc("zc_read_pinned_to_hbm", hin, dbuf, total, b, 1024);
         zc("zc_write_hbm_to_pinned", dbuf, hout, total, b, 1024);
         zc("zc_pinned_to_pinned", hin, hout, total, b, 1024);
+    }
+    cudaFuncSetAttribute(noop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 196480);
+    for (size_t c : {8ull << 20, 16ull << 20}) {
+        run("copies_events", hin, hout, stage, 3, total, c, false, true, sh, sk, sd, 0);
+        g_kernel_kind = 0;
+        run("touch_kernel_events", hin, hout, stage, 3, total, c, true, true, sh, sk, sd, 0);
+        g_kernel_kind = 1;
+        run("noop148x1024_kernel_events", hin, hout, stage, 3, total, c, true, true, sh, sk, sd, 0);
+        run("noop148x1024_192KB_kernel_events", hin, hout, stage, 3, total, c, true, true, sh, sk, sd, 196480);
+        g_kernel_kind = 2;
+        run("noop1x32_kernel_events", hin, hout, stage, 3, total, c, true, true, sh, sk, sd, 0);
+        g_kernel_kind = 0;
     }
     for (size_t c : {1ull << 20, 4ull << 20, 8ull << 20, 16ull << 20}) {
         hybrid("ce_h2d+kernel_writes_host", true, hin, hout, stage, 3, total, c, sh, sk);
