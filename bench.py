@@ -133,6 +133,33 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def duplex_link_gbs(torch, h_a, h_b, nbytes=128 << 20, reps=5):
+    """Measured concurrent H2D + D2H pinned copy bandwidth per direction (the
+    pinned-host path's roofline: every payload byte crosses the link both ways)."""
+    nbytes = min(nbytes, h_a.numel(), h_b.numel())
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s1.wait_event(e0)
+        s2.wait_event(e0)
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a[:nbytes], non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_b[:nbytes].copy_(d_b, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        best = t if best is None else min(best, t)
+    return nbytes / best / 1e9
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -312,6 +339,10 @@ def run_ours(args):
         e2e = {"value": bytes_step * e_steps * world / te / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": bytes_step + 16 * n, "d2h_bytes_per_step": bytes_step,
                "steps": e_steps, "residency": "pinned host (cudaHostAlloc via torch pin_memory)"}
+        # host-link roofline for this path: pinned H2D and D2H copy engines at once
+        link = duplex_link_gbs(torch, hx, hout)
+        e2e["link_duplex_gbs_per_direction"] = link
+        e2e["link_frac"] = (e2e["value"] / world) / link if link else None
         del hx, hout, hiv
 
     if rank != 0:
@@ -327,6 +358,7 @@ def run_ours(args):
         "bound": "alu", "pipe": "lds (shared-memory T-table lookups: 16*Nr lane-lookups per 16-byte block)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": load_traffic(args.workload),
+        "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/traffic.json)",
         "peak_basis": f"{SM_COUNT} SMs x {sm_max:.0f} MHz (sm_max) x {LDS_LANES_PER_CLK} lane-lookups/clk/SM / (16*Nr lookups per 16 B)",
         "frac_at_measured_clock": (achieved / compute_peak_gbs(key_bytes, clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
         "hbm_payload_peak": peaks["hbm_gbs"] / (2 + 16.0 / PB),
