@@ -26,7 +26,7 @@ MAX_INFLIGHT = 65536
 #: every symbol include/kg.h declares
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
                "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path",
-               "kg_nsk_start", "kg_nsk_stop", "kg_nsk_dispatch")
+               "kg_nsk_start", "kg_nsk_stop", "kg_nsk_dispatch", "kg_alloc_pinned", "kg_free_pinned")
 NSK_DIRECT = 1
 HOST_STAGED, HOST_ZEROCOPY, HOST_AUTO = 0, 1, 2
 
@@ -60,6 +60,10 @@ _lib.kg_nsk_stop.argtypes = []
 _lib.kg_nsk_stop.restype = ctypes.c_int
 _lib.kg_nsk_dispatch.argtypes = [ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
 _lib.kg_nsk_dispatch.restype = ctypes.c_int
+_lib.kg_alloc_pinned.argtypes = [ctypes.c_uint64]
+_lib.kg_alloc_pinned.restype = ctypes.c_void_p
+_lib.kg_free_pinned.argtypes = [ctypes.c_void_p]
+_lib.kg_free_pinned.restype = ctypes.c_int
 _lib.kg_launch_count.argtypes = []
 _lib.kg_launch_count.restype = ctypes.c_uint64
 
@@ -168,6 +172,23 @@ def nsk_dispatch(max_bytes: int = 0) -> int:
     out = ctypes.c_uint64(0)
     _check(_lib.kg_nsk_dispatch(int(max_bytes), ctypes.byref(out)), "kg_nsk_dispatch")
     return int(out.value)
+
+
+def alloc_pinned(nbytes: int):
+    """NUMA-local pinned+mapped host buffer as a torch uint8 tensor (freed with free_pinned)."""
+    import torch
+    p = _lib.kg_alloc_pinned(int(nbytes))
+    if not p:
+        raise KgError(ENOMEM, "kg_alloc_pinned")
+    buf = (ctypes.c_uint8 * int(nbytes)).from_address(p)
+    t = torch.frombuffer(buf, dtype=torch.uint8)
+    t._kg_base = p  # noqa: SLF001  (keeps the base address for free_pinned)
+    return t
+
+
+def free_pinned(t) -> None:
+    base = getattr(t, "_kg_base", None)
+    _check(_lib.kg_free_pinned(base if base is not None else _addr(t)), "kg_free_pinned")
 
 
 def launch_count() -> int:

@@ -24,10 +24,13 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <sched.h>
+#include <sys/mman.h>
 #include <time.h>
 
 #include <atomic>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -567,6 +570,91 @@ int kg_set_pipeline(uint64_t chunk_bytes, int slots) {
         g.n_slots = slots;
     }
     g.chunk_bytes = chunk_bytes;
+    return KG_OK;
+}
+
+// ---- pinned host allocations (row f4: "let subsystems allocate memory in the
+// pinned region") -------------------------------------------
+// NUMA placement without libnuma: the pages are first-touched by threads bound
+// to the CPUs local to the GPU's PCI device (sysfs local_cpulist), so the
+// kernel's default local-allocation policy puts them on the GPU's node; then
+// the range is registered (pinned + mapped) with CUDA.
+namespace {
+std::unordered_map<void *, uint64_t> g_pinned;  // base -> bytes (guarded by g_mu)
+
+bool local_cpus(int device, cpu_set_t *set) {
+    char bus[32];
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    for (char *c = bus; *c; ++c)
+        if (*c >= 'A' && *c <= 'F') *c = (char)(*c - 'A' + 'a');
+    char path[128];
+    snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/local_cpulist", bus);
+    FILE *f = fopen(path, "r");
+    if (!f) return false;
+    char buf[1024];
+    const bool ok = fgets(buf, sizeof buf, f) != nullptr;
+    fclose(f);
+    if (!ok) return false;
+    CPU_ZERO(set);
+    int n = 0;
+    for (char *tok = strtok(buf, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+        int a = -1, b = -1;
+        if (sscanf(tok, "%d-%d", &a, &b) == 2) {
+        } else if (sscanf(tok, "%d", &a) == 1) {
+            b = a;
+        } else {
+            continue;
+        }
+        for (int c = a; c <= b && c < CPU_SETSIZE; c++, n++) CPU_SET(c, set);
+    }
+    return n > 0;
+}
+}  // namespace
+
+void *kg_alloc_pinned(uint64_t bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.up || bytes == 0) return nullptr;
+    const uint64_t align = 2ull << 20;
+    const uint64_t len = (bytes + align - 1) / align * align;
+    void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (p == MAP_FAILED) return nullptr;
+    madvise(p, len, MADV_HUGEPAGE);
+    cpu_set_t local;
+    const bool have_local = local_cpus(g.device, &local);
+    unsigned nthr = have_local ? (unsigned)CPU_COUNT(&local) : std::thread::hardware_concurrency();
+    if (nthr < 1) nthr = 1;
+    if (nthr > 16) nthr = 16;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nthr; t++) {
+        th.emplace_back([=, &local] {
+            if (have_local) sched_setaffinity(0, sizeof local, &local);
+            const uint64_t pages = len / 4096;
+            const uint64_t lo = pages * t / nthr, hi = pages * (t + 1) / nthr;
+            volatile uint8_t *b = (volatile uint8_t *)p;
+            for (uint64_t i = lo; i < hi; i++) b[i * 4096] = 0;  // first touch on the local node
+        });
+    }
+    for (auto &x : th) x.join();
+    if (cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, len);
+        return nullptr;
+    }
+    g_pinned[p] = len;
+    return p;
+}
+
+int kg_free_pinned(void *p) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_pinned.find(p);
+    if (it == g_pinned.end()) return KG_EINVAL;
+    cudaHostUnregister(p);
+    cudaGetLastError();
+    munmap(p, it->second);
+    g_pinned.erase(it);
     return KG_OK;
 }
 

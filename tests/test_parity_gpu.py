@@ -127,3 +127,32 @@ def test_cbc_host_zero_copy(direction, n, pb, mode):
     assert first_mismatch(got, exp) is None
     assert first_mismatch(got_ip, exp) is None
     assert first_mismatch(got_mixed, exp) is None
+
+
+def test_alloc_pinned_numa_buffers():
+    """Row f4: library-allocated NUMA-local pinned buffers work as batch memory
+    on both host paths and round-trip through free."""
+    from gpu_util import kg_ready
+    kg, torch = kg_ready()
+    n, pb = 2048, 4096
+    key = synth.make_key(16, seed=91)
+    kg.set_key(0, key)
+    data = synth.make_pages(n, pb, seed=92)
+    ivs = synth.make_ivs(n, seed=93)
+    exp = oracle_pages(1, 0, key, data, n, pb, ivs)
+    hin = kg.alloc_pinned(n * pb)
+    hout = kg.alloc_pinned(n * pb)
+    hiv = kg.alloc_pinned(16 * n)
+    try:
+        hin.copy_(torch.from_numpy(data))
+        hiv.copy_(torch.from_numpy(ivs))
+        for hp in (kg.HOST_STAGED, kg.HOST_ZEROCOPY):
+            kg.set_host_path(hp)
+            hout.zero_()
+            kg.wait(kg.submit_pages(1, 0, hin, hout, n, pb, hiv, 0))
+            assert first_mismatch(hout.numpy(), exp) is None, hp
+    finally:
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)
+        for t in (hin, hout, hiv):
+            kg.free_pinned(t)
+    assert kg.raw_lib().kg_free_pinned(12345) == kg.EINVAL
