@@ -121,9 +121,24 @@ KG_API int64_t kg_submit_pages(int dir, int mode, const void *in, void *out,
                         uint64_t n_pages, uint32_t page_bytes,
                         const void *ivs, int key_id, void *stream);
 
+/* Mixed-key batch (row f1 extension: one batch serves "a number of smaller
+ * blocks of different tasks"): as kg_submit_pages, but page
+ * p uses key key_ids[p] (uint16 per page, 2-byte aligned, device or pinned
+ * host memory).  Every referenced key must be set and key_bytes long; the
+ * key table is snapshotted at submit.  Host buffers are read/written in place
+ * (zero-copy).  A page naming an unset key or a key of another size makes
+ * kg_wait return KG_ENOKEY (that page's output is unspecified).
+ * Errors: as kg_submit_pages, plus KG_EINVAL for bad key_bytes or key_ids,
+ * KG_ENOTSUP while the NSK runs. */
+KG_API int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out,
+                                     uint64_t n_pages, uint32_t page_bytes,
+                                     const void *ivs, const uint16_t *key_ids, int key_bytes,
+                                     void *stream);
+
 /* Block until the batch of `ticket` has completed; retire the ticket.
  * Returns KG_OK, KG_ECUDA (an asynchronous device fault), KG_ETICKET
- * (unknown / already retired / being waited on by another thread). */
+ * (unknown / already retired / being waited on by another thread), KG_ENOKEY
+ * (mixed-key batch naming an unset / other-size key). */
 KG_API int kg_wait(int64_t ticket);
 
 /* Non-blocking completion check (the paper's busy-wait mode).

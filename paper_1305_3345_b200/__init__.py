@@ -26,7 +26,8 @@ MAX_INFLIGHT = 65536
 #: every symbol include/kg.h declares
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
                "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path",
-               "kg_nsk_start", "kg_nsk_stop", "kg_nsk_dispatch", "kg_alloc_pinned", "kg_free_pinned")
+               "kg_nsk_start", "kg_nsk_stop", "kg_nsk_dispatch", "kg_alloc_pinned", "kg_free_pinned",
+               "kg_submit_pages_keyed")
 NSK_DIRECT = 1
 HOST_STAGED, HOST_ZEROCOPY, HOST_AUTO = 0, 1, 2
 
@@ -42,6 +43,9 @@ _lib.kg_set_key.restype = ctypes.c_int
 _lib.kg_submit_pages.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                  ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 _lib.kg_submit_pages.restype = ctypes.c_int64
+_lib.kg_submit_pages_keyed.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                       ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+_lib.kg_submit_pages_keyed.restype = ctypes.c_int64
 _lib.kg_wait.argtypes = [ctypes.c_int64]
 _lib.kg_wait.restype = ctypes.c_int
 _lib.kg_poll.argtypes = [ctypes.c_int64]
@@ -127,6 +131,14 @@ def submit_pages_raw(direction, mode, inp, out, n_pages, page_bytes, ivs, key_id
     """Like submit_pages but returns the raw status/ticket without raising."""
     return _lib.kg_submit_pages(int(direction), int(mode), _addr(inp), _addr(out), int(n_pages), int(page_bytes),
                                 _addr(ivs), int(key_id), _stream(stream))
+
+
+def submit_pages_keyed(direction: int, mode: int, inp, out, n_pages: int, page_bytes: int, ivs, key_ids,
+                       key_bytes: int, stream=None) -> int:
+    """Mixed-key batch: page p under key key_ids[p] (uint16 tensor); returns the ticket."""
+    rc = _lib.kg_submit_pages_keyed(int(direction), int(mode), _addr(inp), _addr(out), int(n_pages), int(page_bytes),
+                                    _addr(ivs), _addr(key_ids), int(key_bytes), _stream(stream))
+    return _check(rc, "kg_submit_pages_keyed")
 
 
 def wait(ticket: int) -> None:

@@ -76,6 +76,19 @@ struct NskCtl {                       // device memory, private to the NSK
 };
 static_assert(offsetof(NskRing, req) % 16 == 0 && offsetof(NskCtl, req) % 16 == 0, "aligned request slots");
 
+// ---- mixed-key batches (row f1 extension) ------------------
+constexpr int kMaxKeys = 256;
+struct DevKeyTable {                 // a snapshot of the whole key table (device)
+    uint4 enc[kMaxKeys][15];         // RoundKeys.w as uint4 per round
+    uint4 dec[kMaxKeys][15];
+    uint8_t nr[kMaxKeys];            // 0 = key id not set
+};
+struct KeyedArgs {
+    const uint16_t *key_ids;         // [n_pages] key id per page (device-usable address)
+    const DevKeyTable *tab;
+    uint32_t *status;                // set to nonzero if a page names an unset / other-size key
+};
+
 // kg_tables.cpp
 void build_base_tables(BaseTables *t);
 int expand_key(const uint8_t *key, int key_bytes, RoundKeys *enc, RoundKeys *dec);  // returns Nr or -1
@@ -84,6 +97,9 @@ int expand_key(const uint8_t *key, int key_bytes, RoundKeys *enc, RoundKeys *dec
 cudaError_t kernels_init(const BaseTables &t);
 // Enqueue one batch on `st`.  dir/mode/nr validated by the caller.
 cudaError_t launch_pages(int dir, int mode, int nr, const LaunchArgs &a, int num_sms, cudaStream_t st);
+// Mixed-key batch: page p uses key k.key_ids[p] (all of size nr).
+cudaError_t launch_pages_keyed(int dir, int mode, int nr, const LaunchArgs &a, const KeyedArgs &k, int num_sms,
+                               cudaStream_t st);
 // Launch the NSK cooperatively with `ctas` CTAs; it expects request seq0 next
 // and exits after idle_ns without a posted request (or on a quit request).
 cudaError_t launch_nsk(NskRing *ring_dev, NskCtl *ctl, uint64_t seq0, uint64_t idle_ns, int ctas, cudaStream_t st);

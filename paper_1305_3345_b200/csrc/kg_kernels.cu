@@ -199,21 +199,26 @@ __device__ __forceinline__ uint32_t lane_bytes() {
 // first(x) = x ^ round key 0; rounds(s) = the remaining Nr rounds (through the
 // final AddRoundKey).  Param*: keys by value in the kernel parameter (constant
 // bank operands).  The NSK (kg_nsk.cuh) supplies shared-memory-key policies.
+// lane(page) returns the per-lane key context of a block of `page` (empty
+// unless keys vary per page: the mixed-key policies below).
+struct NoLane {};
 template <int NR>
 struct ParamEnc {
     const char *sm;
     uint32_t lb;
     const RoundKeys &k;
-    __device__ __forceinline__ uint4 first(uint4 x) const { return xor4k(x, k, 0); }
-    __device__ __forceinline__ uint4 rounds(uint4 s) const { return encrypt_rounds<NR>(sm, lb, s, k); }
+    __device__ __forceinline__ NoLane lane(uint64_t) const { return {}; }
+    __device__ __forceinline__ uint4 first(NoLane, uint4 x) const { return xor4k(x, k, 0); }
+    __device__ __forceinline__ uint4 rounds(NoLane, uint4 s) const { return encrypt_rounds<NR>(sm, lb, s, k); }
 };
 template <int NR>
 struct ParamDec {
     const char *sm;
     uint32_t lb;
     const RoundKeys &k;
-    __device__ __forceinline__ uint4 first(uint4 x) const { return xor4k(x, k, 0); }
-    __device__ __forceinline__ uint4 rounds(uint4 s) const { return decrypt_rounds<NR>(sm, lb, s, k); }
+    __device__ __forceinline__ NoLane lane(uint64_t) const { return {}; }
+    __device__ __forceinline__ uint4 first(NoLane, uint4 x) const { return xor4k(x, k, 0); }
+    __device__ __forceinline__ uint4 rounds(NoLane, uint4 s) const { return decrypt_rounds<NR>(sm, lb, s, k); }
 };
 
 // One batch (or one CTA's share of it): where the pages are.
@@ -277,7 +282,8 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
             carry = r;
             if (act && j == 0) prev = a.ivs[page];
         }
-        uint4 o = cph.rounds(cph.first(c));
+        const auto kl = cph.lane(page);
+        uint4 o = cph.rounds(kl, cph.first(kl, c));
         if (CBC && DEC) o = xor4(o, prev);
         if (act) st_stream(a.out + g, o);
         // advance (page, j) by 32 blocks
@@ -338,8 +344,9 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
             carry = r;
             if (act && jp == 0) prev = a.ivs[page];
         }
-        uint4 o0 = cph.rounds(cph.first(x0));
-        uint4 o1 = cph.rounds(cph.first(x1));
+        const auto kl = cph.lane(page);
+        uint4 o0 = cph.rounds(kl, cph.first(kl, x0));
+        uint4 o1 = cph.rounds(kl, cph.first(kl, x1));
         if (CBC && DEC) {
             o0 = xor4(o0, prev);
             o1 = xor4(o1, x0);
@@ -369,6 +376,7 @@ __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, ui
         const uint4 *src = a.in + p * m;
         uint4 *dst = a.out + p * m;
         uint4 prev = a.ivs[p];  // C_{p,-1} := IV_p
+        const auto kl = cph.lane(p);
         if (WIDE) {
             uint4 x0, x1;
             ld256<true>(src, x0, x1);
@@ -376,8 +384,8 @@ __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, ui
                 uint4 n0 = x0, n1 = x1;
                 if (j + 2 < m) ld256<true>(src + j + 2, n0, n1);  // prefetch P_{j+2}, P_{j+3}
                 // C_j = E_K(P_j ^ C_{j-1}); the first AddRoundKey folds into the same XOR
-                const uint4 c0 = cph.rounds(cph.first(xor4(x0, prev)));
-                prev = cph.rounds(cph.first(xor4(x1, c0)));
+                const uint4 c0 = cph.rounds(kl, cph.first(kl, xor4(x0, prev)));
+                prev = cph.rounds(kl, cph.first(kl, xor4(x1, c0)));
                 st256<true>(dst + j, c0, prev);
                 x0 = n0;
                 x1 = n1;
@@ -387,7 +395,7 @@ __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, ui
             for (uint32_t j = 0; j < m; ++j) {
                 uint4 xn = x;
                 if (j + 1 < m) xn = src[j + 1];  // prefetch P_{j+1} (read before C_j is stored)
-                prev = cph.rounds(cph.first(xor4(x, prev)));
+                prev = cph.rounds(kl, cph.first(kl, xor4(x, prev)));
                 dst[j] = prev;
                 x = xn;
             }
@@ -433,6 +441,104 @@ __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant_
     cbc_enc_body<WIDE>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
 }
 
+// ---- mixed-key batches -------------------------------------------------------
+// Round keys come from a device snapshot of the key table, per lane (the key of
+// the lane's page), one 16-byte load per round; lanes of a warp usually share
+// a page, so the loads broadcast.
+template <int NR>
+__device__ __forceinline__ uint4 keyed_encrypt_rounds(const char *sm, uint32_t lb, uint4 s, const uint4 *k) {
+    uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+        const uint4 kr = __ldg(k + r);
+        const uint32_t t0 = T<0>(sm, s0, lb) ^ T<1>(sm, s1, lb) ^ T<2>(sm, s2, lb) ^ T<3>(sm, s3, lb) ^ kr.x;
+        const uint32_t t1 = T<0>(sm, s1, lb) ^ T<1>(sm, s2, lb) ^ T<2>(sm, s3, lb) ^ T<3>(sm, s0, lb) ^ kr.y;
+        const uint32_t t2 = T<0>(sm, s2, lb) ^ T<1>(sm, s3, lb) ^ T<2>(sm, s0, lb) ^ T<3>(sm, s1, lb) ^ kr.z;
+        const uint32_t t3 = T<0>(sm, s3, lb) ^ T<1>(sm, s0, lb) ^ T<2>(sm, s1, lb) ^ T<3>(sm, s2, lb) ^ kr.w;
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    const uint4 kl = __ldg(k + NR);
+    uint4 o;
+#define KG_ENC_LAST(dst, a, b, c, d, kw)                                                                  \
+    dst = __byte_perm(__byte_perm(T<0>(sm, a, lb), T<1>(sm, b, lb), 0x0061u),                             \
+                      __byte_perm(T<2>(sm, c, lb), T<3>(sm, d, lb), 0x4300u), 0x7610u) ^ kw;
+    KG_ENC_LAST(o.x, s0, s1, s2, s3, kl.x)
+    KG_ENC_LAST(o.y, s1, s2, s3, s0, kl.y)
+    KG_ENC_LAST(o.z, s2, s3, s0, s1, kl.z)
+    KG_ENC_LAST(o.w, s3, s0, s1, s2, kl.w)
+#undef KG_ENC_LAST
+    return o;
+}
+
+template <int NR>
+__device__ __forceinline__ uint4 keyed_decrypt_rounds(const char *sm, uint32_t lb, uint4 s, const uint4 *k) {
+    uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+        const uint4 kr = __ldg(k + r);
+        const uint32_t t0 = T<0>(sm, s0, lb) ^ T<1>(sm, s3, lb) ^ T<2>(sm, s2, lb) ^ T<3>(sm, s1, lb) ^ kr.x;
+        const uint32_t t1 = T<0>(sm, s1, lb) ^ T<1>(sm, s0, lb) ^ T<2>(sm, s3, lb) ^ T<3>(sm, s2, lb) ^ kr.y;
+        const uint32_t t2 = T<0>(sm, s2, lb) ^ T<1>(sm, s1, lb) ^ T<2>(sm, s0, lb) ^ T<3>(sm, s3, lb) ^ kr.z;
+        const uint32_t t3 = T<0>(sm, s3, lb) ^ T<1>(sm, s2, lb) ^ T<2>(sm, s1, lb) ^ T<3>(sm, s0, lb) ^ kr.w;
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    const uint4 kl = __ldg(k + NR);
+    uint4 o;
+#define KG_DEC_LAST(dst, a, b, c, d, kw)                                                                  \
+    dst = __byte_perm(__byte_perm(IS<0>(sm, a, lb), IS<1>(sm, b, lb), 0x0040u),                           \
+                      __byte_perm(IS<2>(sm, c, lb), IS<3>(sm, d, lb), 0x4000u), 0x7610u) ^ kw;
+    KG_DEC_LAST(o.x, s0, s3, s2, s1, kl.x)
+    KG_DEC_LAST(o.y, s1, s0, s3, s2, kl.y)
+    KG_DEC_LAST(o.z, s2, s1, s0, s3, kl.z)
+    KG_DEC_LAST(o.w, s3, s2, s1, s0, kl.w)
+#undef KG_DEC_LAST
+    return o;
+}
+
+template <int NR, bool DEC>
+struct KeyedPolicy {
+    const char *sm;
+    uint32_t lb;
+    const uint4 (*tab)[15];  // enc or dec schedules of the snapshot
+    const uint8_t *nr;
+    const uint16_t *ids;
+    uint32_t *status;
+    uint64_t n_pages;
+    struct L {
+        const uint4 *k;
+    };
+    __device__ __forceinline__ L lane(uint64_t page) const {
+        if (page >= n_pages) page = n_pages - 1;  // inactive tail lanes
+        uint32_t id = __ldg(ids + page);
+        if (id >= (uint32_t)kMaxKeys || nr[id] != NR) {
+            atomicOr(status, 1u);
+            id = 0;
+        }
+        return L{tab[id]};
+    }
+    __device__ __forceinline__ uint4 first(L l, uint4 x) const { return xor4(x, __ldg(l.k)); }
+    __device__ __forceinline__ uint4 rounds(L l, uint4 s) const {
+        return DEC ? keyed_decrypt_rounds<NR>(sm, lb, s, l.k) : keyed_encrypt_rounds<NR>(sm, lb, s, l.k);
+    }
+};
+
+template <int NR, int DIR, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) kg_keyed(const __grid_constant__ LaunchArgs a, KeyedArgs k) {
+    extern __shared__ __align__(16) char sm[];
+    constexpr bool DEC = (DIR == 1);
+    constexpr bool CBC = (MODE == 0);
+    fill_tables<DEC>(sm);
+    pdl_prologue_done();
+    const uint32_t lb = lane_bytes();
+    const KeyedPolicy<NR, DEC> pol{sm, lb, DEC ? k.tab->dec : k.tab->enc, k.tab->nr, k.key_ids, k.status, a.n_pages};
+    if (!DEC && CBC) {
+        __syncthreads();
+        cbc_enc_body<false>(job_of(a), pol, blockIdx.x, gridDim.x);
+    } else {
+        blockpar_body<DEC, CBC>(job_of(a), pol, blockIdx.x, gridDim.x);
+    }
+}
+
 #include "kg_nsk.cuh"
 
 template <typename K>
@@ -451,12 +557,16 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_blockpar<NR, 0, 1, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, false>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed<NR, 1, 0>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed<NR, 1, 1>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed<NR, 0, 1>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed<NR, 0, 0>, kSmemEnc)) != cudaSuccess) return e;
     return cudaSuccess;
 }
 
 // Launch with the programmatic-stream-serialization attribute (PDL).
-template <typename... KArgs>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaStream_t st, const LaunchArgs &a) {
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaStream_t st, const Args &...args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -471,7 +581,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaSt
         return (e && *e == '0') ? 0 : 1;
     }();
     cfg.numAttrs = use_pdl;
-    return cudaLaunchKernelEx(&cfg, kernel, a);
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 template <int NR>
@@ -501,7 +611,31 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
     return launch_pdl(kg_blockpar<NR, 0, 1, false>, grid, kSmemEnc, st, a);
 }
 
+template <int NR>
+cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedArgs &k, int num_sms, cudaStream_t st) {
+    const uint64_t nb = a.n_pages * (uint64_t)a.m;
+    uint64_t want = (dir == 0 && mode == 0) ? a.n_pages : (nb + 255) / 256;
+    if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
+    if (a.in_place && want > a.n_pages) want = a.n_pages;
+    if (want < 1) want = 1;
+    const unsigned grid = (unsigned)want;
+    if (dir == 1 && mode == 0) return launch_pdl(kg_keyed<NR, 1, 0>, grid, kSmemDec, st, a, k);
+    if (dir == 1) return launch_pdl(kg_keyed<NR, 1, 1>, grid, kSmemDec, st, a, k);
+    if (mode == 1) return launch_pdl(kg_keyed<NR, 0, 1>, grid, kSmemEnc, st, a, k);
+    return launch_pdl(kg_keyed<NR, 0, 0>, grid, kSmemEnc, st, a, k);
+}
+
 }  // namespace
+
+cudaError_t launch_pages_keyed(int dir, int mode, int nr, const LaunchArgs &a, const KeyedArgs &k, int num_sms,
+                               cudaStream_t st) {
+    switch (nr) {
+        case 10: return launch_keyed_nr<10>(dir, mode, a, k, num_sms, st);
+        case 12: return launch_keyed_nr<12>(dir, mode, a, k, num_sms, st);
+        case 14: return launch_keyed_nr<14>(dir, mode, a, k, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
 
 cudaError_t kernels_init(const BaseTables &t) {
     cudaError_t e = cudaMemcpyToSymbol(g_tables, &t, sizeof(BaseTables));

@@ -136,16 +136,18 @@ struct SmemEnc {
     const char *sm;
     uint32_t lb;
     const uint4 *ks;
-    __device__ __forceinline__ uint4 first(uint4 x) const { return xor4(x, ks[0]); }
-    __device__ __forceinline__ uint4 rounds(uint4 s) const { return nsk_encrypt_rounds<NR>(sm, lb, s, ks); }
+    __device__ __forceinline__ NoLane lane(uint64_t) const { return {}; }
+    __device__ __forceinline__ uint4 first(NoLane, uint4 x) const { return xor4(x, ks[0]); }
+    __device__ __forceinline__ uint4 rounds(NoLane, uint4 s) const { return nsk_encrypt_rounds<NR>(sm, lb, s, ks); }
 };
 template <int NR>
 struct SmemDec {
     const char *sm;
     uint32_t lb;
     const uint4 *ks;
-    __device__ __forceinline__ uint4 first(uint4 x) const { return xor4(x, ks[0]); }
-    __device__ __forceinline__ uint4 rounds(uint4 s) const { return nsk_decrypt_rounds<NR>(sm, lb, s, ks); }
+    __device__ __forceinline__ NoLane lane(uint64_t) const { return {}; }
+    __device__ __forceinline__ uint4 first(NoLane, uint4 x) const { return xor4(x, ks[0]); }
+    __device__ __forceinline__ uint4 rounds(NoLane, uint4 s) const { return nsk_decrypt_rounds<NR>(sm, lb, s, ks); }
 };
 
 template <int NR>

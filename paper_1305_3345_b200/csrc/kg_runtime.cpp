@@ -48,6 +48,7 @@ struct KeySlot {
 struct Ticket {
     cudaEvent_t ev = nullptr;     // launch/staged batches: completion event
     bool claimed = false;
+    int status_slot = -1;         // mixed-key batches: pinned status word
     uint64_t nsk_seq = 0;         // NSK requests: sequence number (ev == nullptr)
     uint64_t nsk_gen = 0;         // NSK lifetime the request belongs to
 };
@@ -79,6 +80,8 @@ struct Slot {
 };
 
 constexpr int kMaxSlots = 8;
+constexpr int kKeySnaps = 4;
+constexpr uint32_t kStatusSlots = 1024;
 constexpr uint64_t kIvStageMax = 256ull << 20;  // IVs of up to 16M pages (64 GiB of 4 KiB pages)
 
 struct Ctx {
@@ -101,6 +104,19 @@ struct Ctx {
     int host_path = KG_HOST_AUTO;
     uint64_t zc_max_bytes = 32ull << 20;  // zero-copy beats staging up to 32 MiB (tools/sweep.py, r1p)
     Nsk nsk;
+    // mixed-key batches: host mirror of the key table, device snapshot ring,
+    // pinned status words
+    kg::DevKeyTable *ktab_host = nullptr;              // pinned, updated by kg_set_key
+    uint64_t key_version = 1;
+    kg::DevKeyTable *ktab_stage[kKeySnaps] = {};       // pinned staging copies
+    kg::DevKeyTable *ktab_dev[kKeySnaps] = {};
+    uint64_t ktab_dev_version[kKeySnaps] = {};
+    cudaEvent_t ktab_used[kKeySnaps] = {};
+    int ktab_cur = -1;
+    uint32_t *status = nullptr;                        // pinned mapped, kStatusSlots words
+    uint32_t *status_dev = nullptr;
+    bool status_busy[kStatusSlots] = {};
+    uint32_t status_next = 0;
     PFN_writeValue64 write_value64 = nullptr;
     PFN_waitValue64 wait_value64 = nullptr;
 };
@@ -677,6 +693,12 @@ int kg_set_key(int key_id, const uint8_t *key, int key_bytes) {
     if (ks.nr < 0) return KG_EINVAL;
     ks.set = true;
     g.keys[key_id] = ks;
+    if (g.ktab_host) {
+        memcpy(g.ktab_host->enc[key_id], ks.enc.w, sizeof(g.ktab_host->enc[key_id]));
+        memcpy(g.ktab_host->dec[key_id], ks.dec.w, sizeof(g.ktab_host->dec[key_id]));
+        g.ktab_host->nr[key_id] = (uint8_t)ks.nr;
+        g.key_version++;
+    }
     return KG_OK;
 }
 
@@ -749,6 +771,133 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
     return new_ticket(st);
 }
 
+// ---- mixed-key batches ------------------------------------------------------------
+static int keyed_setup() {
+    if (g.ktab_host) return KG_OK;
+    if (cudaHostAlloc((void **)&g.ktab_host, sizeof(kg::DevKeyTable), 0) != cudaSuccess) goto fail;
+    memset(g.ktab_host, 0, sizeof(kg::DevKeyTable));
+    for (int i = 0; i < KG_MAX_KEYS; i++)
+        if (g.keys[i].set) {
+            memcpy(g.ktab_host->enc[i], g.keys[i].enc.w, sizeof(g.ktab_host->enc[i]));
+            memcpy(g.ktab_host->dec[i], g.keys[i].dec.w, sizeof(g.ktab_host->dec[i]));
+            g.ktab_host->nr[i] = (uint8_t)g.keys[i].nr;
+        }
+    for (int i = 0; i < kKeySnaps; i++) {
+        if (cudaHostAlloc((void **)&g.ktab_stage[i], sizeof(kg::DevKeyTable), 0) != cudaSuccess) goto fail;
+        if (cudaMalloc((void **)&g.ktab_dev[i], sizeof(kg::DevKeyTable)) != cudaSuccess) goto fail;
+        if (cudaEventCreateWithFlags(&g.ktab_used[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+        g.ktab_dev_version[i] = 0;
+    }
+    if (cudaHostAlloc((void **)&g.status, kStatusSlots * sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) goto fail;
+    if (cudaHostGetDevicePointer((void **)&g.status_dev, g.status, 0) != cudaSuccess) goto fail;
+    memset(g.status, 0, kStatusSlots * sizeof(uint32_t));
+    return KG_OK;
+fail:
+    cudaGetLastError();
+    return KG_ENOMEM;
+}
+
+static void keyed_teardown() {
+    if (g.ktab_host) cudaFreeHost(g.ktab_host);
+    for (int i = 0; i < kKeySnaps; i++) {
+        if (g.ktab_stage[i]) cudaFreeHost(g.ktab_stage[i]);
+        if (g.ktab_dev[i]) cudaFree(g.ktab_dev[i]);
+        if (g.ktab_used[i]) cudaEventDestroy(g.ktab_used[i]);
+        g.ktab_stage[i] = nullptr;
+        g.ktab_dev[i] = nullptr;
+        g.ktab_used[i] = nullptr;
+    }
+    if (g.status) cudaFreeHost(g.status);
+    g.ktab_host = nullptr;
+    g.status = g.status_dev = nullptr;
+    g.ktab_cur = -1;
+    for (auto &b : g.status_busy) b = false;
+}
+
+// A device snapshot of the current key table, uploaded on `st` if keys changed.
+static int keyed_snapshot(cudaStream_t st, const kg::DevKeyTable **out) {
+    if (g.ktab_cur >= 0 && g.ktab_dev_version[g.ktab_cur] == g.key_version) {
+        *out = g.ktab_dev[g.ktab_cur];
+        KG_CU(cudaEventRecord(g.ktab_used[g.ktab_cur], st));
+        return KG_OK;
+    }
+    const int i = (g.ktab_cur + 1) % kKeySnaps;
+    KG_CU(cudaEventSynchronize(g.ktab_used[i]));  // earlier batches done with this snapshot slot
+    memcpy(g.ktab_stage[i], g.ktab_host, sizeof(kg::DevKeyTable));
+    KG_CU(cudaMemcpyAsync(g.ktab_dev[i], g.ktab_stage[i], sizeof(kg::DevKeyTable), cudaMemcpyHostToDevice, st));
+    g.ktab_dev_version[i] = g.key_version;
+    g.ktab_cur = i;
+    KG_CU(cudaEventRecord(g.ktab_used[i], st));
+    *out = g.ktab_dev[i];
+    return KG_OK;
+}
+
+int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint64_t n_pages, uint32_t page_bytes,
+                              const void *ivs, const uint16_t *key_ids, int key_bytes, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.up) return KG_ENOTINIT;
+    if ((dir != KG_ENCRYPT && dir != KG_DECRYPT) || (mode != KG_MODE_CBC && mode != KG_MODE_ECB)) return KG_EINVAL;
+    if (n_pages == 0 || page_bytes == 0 || page_bytes % 16 != 0) return KG_EINVAL;
+    if (n_pages > UINT64_MAX / page_bytes) return KG_EINVAL;
+    if (key_bytes != 16 && key_bytes != 24 && key_bytes != 32) return KG_EINVAL;
+    const uint64_t total = n_pages * page_bytes;
+    const bool need_iv = (mode == KG_MODE_CBC);
+    if (!in || !out || !key_ids || (need_iv && !ivs)) return KG_EINVAL;
+    if ((((uintptr_t)in | (uintptr_t)out) & 15u) || ((uintptr_t)key_ids & 1u)) return KG_EINVAL;
+    if (need_iv && ((uintptr_t)ivs & 15u)) return KG_EINVAL;
+    if (in != out && overlap((uintptr_t)in, total, (uintptr_t)out, total)) return KG_EINVAL;
+    if (need_iv && overlap((uintptr_t)ivs, 16 * n_pages, (uintptr_t)out, total)) return KG_EINVAL;
+    if (overlap((uintptr_t)key_ids, 2 * n_pages, (uintptr_t)out, total)) return KG_EINVAL;
+    if (g.nsk.on) return KG_ENOTSUP;  // the NSK owns SMs; keyed batches use launches only
+    const void *zin = in, *zout = out, *ziv = ivs, *zid = key_ids;
+    const Kind kin = classify(in, &zin), kout = classify(out, &zout), kid = classify(key_ids, &zid),
+               kiv = need_iv ? classify(ivs, &ziv) : K_DEVICE;
+    if (kin == K_BAD || kout == K_BAD || kiv == K_BAD || kid == K_BAD) return KG_EINVAL;
+    // keyed batches run in one launch: host buffers are accessed in place
+    if (!zin || !zout || !zid || (need_iv && !ziv)) return KG_EINVAL;
+    if (g.tickets.size() >= (size_t)KG_MAX_INFLIGHT) return KG_EAGAIN;
+    int rc = keyed_setup();
+    if (rc != KG_OK) return rc;
+    uint32_t sslot = kStatusSlots;
+    for (uint32_t t = 0; t < kStatusSlots; t++) {
+        const uint32_t c = (g.status_next + t) % kStatusSlots;
+        if (!g.status_busy[c]) {
+            sslot = c;
+            break;
+        }
+    }
+    if (sslot == kStatusSlots) return KG_EAGAIN;
+    g.status_next = (sslot + 1) % kStatusSlots;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const kg::DevKeyTable *tab = nullptr;
+    rc = keyed_snapshot(st, &tab);
+    if (rc != KG_OK) return rc;
+    g.status[sslot] = 0;
+    kg::LaunchArgs a;
+    memset(&a.rk, 0, sizeof a.rk);
+    a.in = reinterpret_cast<const uint4 *>(zin);
+    a.out = reinterpret_cast<uint4 *>(const_cast<void *>(zout));
+    a.ivs = need_iv ? reinterpret_cast<const uint4 *>(ziv) : nullptr;
+    a.n_pages = n_pages;
+    a.m = page_bytes / 16;
+    a.in_place = (in == out);
+    kg::KeyedArgs k;
+    k.key_ids = reinterpret_cast<const uint16_t *>(zid);
+    k.tab = tab;
+    k.status = g.status_dev + sslot;
+    const int nr = key_bytes / 4 + 6;
+    const int sms = g.num_sms;
+    cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int64_t t = new_ticket(st);
+    if (t >= 0) {
+        g.tickets[t].status_slot = (int)sslot;
+        g.status_busy[sslot] = true;
+    }
+    return t;
+}
+
 // NSK ticket completion: 1 done, 0 pending, < 0 error.  Caller holds g_mu.
 int nsk_ticket_state(const Ticket &t) {
     if (t.nsk_gen != g.nsk.gen || !g.nsk.on) return 1;  // the NSK was stopped after draining it
@@ -805,10 +954,17 @@ int kg_wait(int64_t ticket) {
     cudaError_t e = cudaEventSynchronize(ev);
     std::lock_guard<std::mutex> lk(g_mu);
     if (trace_on()) trace_dump();
+    int rc = KG_OK;
+    auto it = g.tickets.find(ticket);
+    if (it != g.tickets.end() && it->second.status_slot >= 0) {
+        const int ss = it->second.status_slot;
+        if (e == cudaSuccess && *reinterpret_cast<volatile uint32_t *>(&g.status[ss]) != 0) rc = KG_ENOKEY;
+        g.status_busy[ss] = false;
+    }
     g.tickets.erase(ticket);
     g.ev_pool.push_back(ev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
-    return KG_OK;
+    return rc;
 }
 
 int kg_poll(int64_t ticket) {
@@ -959,6 +1115,7 @@ int kg_shutdown(void) {
     if (!g.up) return KG_ENOTINIT;
     nsk_stop_locked();
     cudaDeviceSynchronize();
+    keyed_teardown();
     for (auto &kv : g.tickets)
         if (kv.second.ev) cudaEventDestroy(kv.second.ev);
     g.tickets.clear();
