@@ -194,7 +194,7 @@ def run_reference(args):
         return 0
     n_pages, key_bytes, direction, _, desc = WORKLOADS[args.workload]
     threads = len(os.sched_getaffinity(0))
-    per_step = max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step = args.ref_step_seconds or max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
     import oracle
     key = synth.make_key(key_bytes)
     # calibrate the per-step sample
@@ -234,12 +234,21 @@ def run_ours(args):
     if not torch.cuda.is_available():
         print(json.dumps({"error": "no CUDA device"}))
         return 1
-    torch.cuda.set_device(local)
+    # one process per GPU; KG_BENCH_SHARE_GPU=1 (testing the N>1 code path on a
+    # one-GPU box) maps ranks onto the available devices and uses gloo
+    share = os.environ.get("KG_BENCH_SHARE_GPU") == "1"
+    dev = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(dev)
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    kg.init(local)
+        if share:
+            dist.init_process_group("gloo")
+            red_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    kg.init(dev)
     n_total, key_bytes, direction, in_place, desc = WORKLOADS[args.workload]
     if args.workload == "c5":
         lo, hi = synth.shard(n_total, rank, world)   # strong scaling: 64 GiB split by page range
@@ -287,7 +296,7 @@ def run_ours(args):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     l0 = kg.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         t_wall0 = time.perf_counter()
         tickets = []
         for i in range(args.steps):
@@ -303,11 +312,9 @@ def run_ours(args):
     per_launch = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
     avg_launch = sum(per_launch) / len(per_launch)
     if dist:
-        t = torch.tensor([elapsed, avg_launch], dtype=torch.float64, device="cuda")
+        t = torch.tensor([elapsed, avg_launch], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed, avg_launch = float(t[0]), float(t[1])
-        bad = torch.zeros(1, dtype=torch.int64, device="cuda")
-        dist.all_reduce(bad, op=dist.ReduceOp.SUM)
     bytes_step = n * PB
     total_bytes = bytes_step * args.steps * (world if scaling == "weak" else 1)
     if scaling == "strong":
@@ -333,7 +340,7 @@ def run_ours(args):
             kg.wait(kg.submit_pages(direction, kg.MODE_CBC, hx, hout, n, PB, hiv, 0, stream))
         te = time.perf_counter() - t0
         if dist:
-            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([te], dtype=torch.float64, device=red_dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt[0])
         e2e = {"value": bytes_step * e_steps * world / te / 1e9, "unit": "GB/s",
@@ -404,6 +411,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=0.0,
+                    help="reference arm: oracle seconds per step (default: sized so the run takes ~2.5 min)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
