@@ -99,8 +99,12 @@ struct Ctx {
     int n_slots = 3;
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
-    uint8_t *iv_stage = nullptr;  // batch IVs of host batches (<= kIvStageMax)
-    uint64_t iv_stage_bytes = 0;
+    // batch IVs of host batches (<= kIvStageMax), double-buffered: a buffer is
+    // reused only after the kernels of the batch that last filled it (iv_free)
+    uint8_t *iv_stage[2] = {nullptr, nullptr};
+    uint64_t iv_stage_bytes[2] = {0, 0};
+    cudaEvent_t iv_free[2] = {nullptr, nullptr};
+    int iv_next = 0;
     int host_path = KG_HOST_AUTO;
     uint64_t zc_max_bytes = 32ull << 20;  // zero-copy beats staging up to 32 MiB (tools/sweep.py, r1p)
     Nsk nsk;
@@ -289,18 +293,18 @@ int launch(int dir, int mode, int nr, const kg::LaunchArgs &a, cudaStream_t st) 
 // the previous chunk's D2H, which delayed every kernel by a whole D2H; reading
 // them in place over the host link slowed the kernels instead
 // (profiles/r1_pinned: trace_*).
-int ensure_iv_stage(uint64_t bytes) {
-    if (g.iv_stage_bytes >= bytes) return KG_OK;
+int ensure_iv_stage(int b, uint64_t bytes) {
+    if (g.iv_stage_bytes[b] >= bytes) return KG_OK;
     cudaStreamSynchronize(g.s_h2d);
     cudaStreamSynchronize(g.s_comp);
-    if (g.iv_stage) cudaFree(g.iv_stage);
-    g.iv_stage = nullptr;
-    g.iv_stage_bytes = 0;
-    if (cudaMalloc(&g.iv_stage, bytes) != cudaSuccess) {
+    if (g.iv_stage[b]) cudaFree(g.iv_stage[b]);
+    g.iv_stage[b] = nullptr;
+    g.iv_stage_bytes[b] = 0;
+    if (cudaMalloc(&g.iv_stage[b], bytes) != cudaSuccess) {
         cudaGetLastError();
         return KG_ENOMEM;
     }
-    g.iv_stage_bytes = bytes;
+    g.iv_stage_bytes[b] = bytes;
     return KG_OK;
 }
 
@@ -320,9 +324,15 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     KG_CU(cudaStreamWaitEvent(g.s_comp, g.ev_begin, 0));
     KG_CU(cudaStreamWaitEvent(g.s_d2h, g.ev_begin, 0));
     // all host IVs in one copy (if they fit the cap), ahead of chunk 0's pages
+    const int ivb = g.iv_next;
     const bool iv_upfront = need_iv && kiv == K_HOST && 16 * n_pages <= kIvStageMax &&
-                            ensure_iv_stage(16 * n_pages) == KG_OK;
-    if (iv_upfront) KG_CU(cudaMemcpyAsync(g.iv_stage, ivs, 16 * n_pages, cudaMemcpyHostToDevice, g.s_h2d));
+                            ensure_iv_stage(ivb, 16 * n_pages) == KG_OK;
+    uint8_t *const iv_buf = iv_upfront ? g.iv_stage[ivb] : nullptr;
+    if (iv_upfront) {
+        g.iv_next ^= 1;
+        KG_CU(cudaStreamWaitEvent(g.s_h2d, g.iv_free[ivb], 0));  // kernels of its previous batch are done
+        KG_CU(cudaMemcpyAsync(iv_buf, ivs, 16 * n_pages, cudaMemcpyHostToDevice, g.s_h2d));
+    }
 
     // Chunk schedule.  The first H2D and the last D2H overlap nothing, so for
     // batches of >= 4 chunks the ends ramp C/8, C/4, C/2 (... C ...) C/2, C/4,
@@ -362,7 +372,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         a.out = reinterpret_cast<uint4 *>(kout == K_HOST ? s.data : out + off);
         a.ivs = !need_iv ? nullptr
                 : reinterpret_cast<const uint4 *>(kiv != K_HOST ? ivs + 16 * p0
-                                                  : iv_upfront ? g.iv_stage + 16 * p0 : s.ivs);
+                                                  : iv_upfront ? iv_buf + 16 * p0 : s.ivs);
         a.n_pages = np;
         a.m = page_bytes / 16;
         a.in_place = (const void *)a.in == (const void *)a.out;
@@ -377,6 +387,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         KG_CU(cudaEventRecord(s.freed, g.s_d2h));
         trace(i, 'd', g.s_d2h);
     }
+    if (iv_upfront) KG_CU(cudaEventRecord(g.iv_free[ivb], g.s_comp));
     // join: the caller's stream continues after the last D2H
     KG_CU(cudaEventRecord(g.ev_begin, g.s_d2h));
     KG_CU(cudaStreamWaitEvent(st, g.ev_begin, 0));
@@ -541,6 +552,7 @@ int kg_init(int device) {
     KG_CU(cudaStreamCreateWithFlags(&g.s_comp, cudaStreamNonBlocking));
     KG_CU(cudaStreamCreateWithFlags(&g.s_d2h, cudaStreamNonBlocking));
     KG_CU(cudaEventCreateWithFlags(&g.ev_begin, cudaEventDisableTiming));
+    for (int b = 0; b < 2; b++) KG_CU(cudaEventCreateWithFlags(&g.iv_free[b], cudaEventDisableTiming));
     for (int i = 0; i < kMaxSlots; i++) {
         KG_CU(cudaEventCreateWithFlags(&g.slots[i].loaded, cudaEventDisableTiming));
         KG_CU(cudaEventCreateWithFlags(&g.slots[i].done, cudaEventDisableTiming));
@@ -1122,9 +1134,13 @@ int kg_shutdown(void) {
     for (cudaEvent_t e : g.ev_pool) cudaEventDestroy(e);
     g.ev_pool.clear();
     free_staging();
-    if (g.iv_stage) cudaFree(g.iv_stage);
-    g.iv_stage = nullptr;
-    g.iv_stage_bytes = 0;
+    for (int b = 0; b < 2; b++) {
+        if (g.iv_stage[b]) cudaFree(g.iv_stage[b]);
+        if (g.iv_free[b]) cudaEventDestroy(g.iv_free[b]);
+        g.iv_stage[b] = nullptr;
+        g.iv_stage_bytes[b] = 0;
+        g.iv_free[b] = nullptr;
+    }
     for (int i = 0; i < kMaxSlots; i++) {
         cudaEventDestroy(g.slots[i].loaded);
         cudaEventDestroy(g.slots[i].done);

@@ -156,3 +156,34 @@ def test_alloc_pinned_numa_buffers():
         for t in (hin, hout, hiv):
             kg.free_pinned(t)
     assert kg.raw_lib().kg_free_pinned(12345) == kg.EINVAL
+
+
+def test_staged_batches_back_to_back():
+    """Several host batches in flight at once through the staging ring (no wait
+    between submits): slots and the double-buffered IV stage must not be
+    reused before their previous users are done."""
+    from gpu_util import kg_ready
+    kg, torch = kg_ready()
+    kg.set_host_path(kg.HOST_STAGED)
+    kg.set_pipeline(64 * 4096, 3)
+    try:
+        n, pb = 700, 4096
+        key = synth.make_key(16, seed=501)
+        kg.set_key(0, key)
+        jobs = []
+        for b in range(6):
+            data = synth.make_pages(n, pb, seed=600 + b)
+            ivs = synth.make_ivs(n, seed=700 + b)
+            d = b % 2
+            hin = torch.from_numpy(data).pin_memory()
+            hiv = torch.from_numpy(ivs).pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            t = kg.submit_pages(d, 0, hin, hout, n, pb, hiv, 0)
+            jobs.append((t, d, data, ivs, hout, hin, hiv))
+        for t, d, data, ivs, hout, *_ in jobs:
+            kg.wait(t)
+            exp = oracle_pages(d, 0, key, data, n, pb, ivs)
+            assert first_mismatch(hout.numpy(), exp) is None
+    finally:
+        kg.set_pipeline(16 << 20, 3)
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)

@@ -8,6 +8,19 @@
 
 #include <vector>
 
+// occupies every SM (1 CTA of 1024 threads + 192 KB smem per SM) for ~`ns`
+__global__ void spin_kernel(unsigned long long ns) {
+    extern __shared__ char smem_dummy[];
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > ns) break;
+    }
+    if (threadIdx.x == 5000) smem_dummy[0] = 1;
+}
+
 __global__ void noop_kernel(uint4 *p, size_t n) {
     if (n == 0xFFFFFFFFFFFull) p[threadIdx.x] = make_uint4(0, 0, 0, 0);
 }
@@ -162,6 +175,35 @@ int main() {
         zc("zc_pinned_to_pinned", hin, hout, total, b, 1024);
     }
     cudaFuncSetAttribute(noop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 196480);
+    cudaFuncSetAttribute(spin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 196480);
+    {
+        // copies (no kernels) while a GPU-filling kernel spins on another stream
+        cudaStream_t sx;
+        cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking);
+        cudaEvent_t a0, a1;
+        cudaEventCreate(&a0);
+        cudaEventCreate(&a1);
+        for (int busy = 0; busy < 2; busy++) {
+            cudaDeviceSynchronize();
+            if (busy) spin_kernel<<<148, 1024, 196480, sx>>>(20000000ull);  // 20 ms
+            cudaEventRecord(a0, sh);
+            cudaMemcpyAsync(stage[0], hin, 64ull << 20, cudaMemcpyHostToDevice, sh);
+            cudaEventRecord(a1, sh);
+            cudaEventSynchronize(a1);
+            float ms;
+            cudaEventElapsedTime(&ms, a0, a1);
+            printf("{\"variant\": \"h2d_64MiB_%s\", \"ms\": %.3f, \"gbs\": %.2f}\n", busy ? "while_gpu_full" : "idle",
+                   ms, (64 << 20) / (ms * 1e-3) / 1e9);
+            cudaEventRecord(a0, sd);
+            cudaMemcpyAsync(hout, stage[1], 64ull << 20, cudaMemcpyDeviceToHost, sd);
+            cudaEventRecord(a1, sd);
+            cudaEventSynchronize(a1);
+            cudaEventElapsedTime(&ms, a0, a1);
+            printf("{\"variant\": \"d2h_64MiB_%s\", \"ms\": %.3f, \"gbs\": %.2f}\n", busy ? "while_gpu_full" : "idle",
+                   ms, (64 << 20) / (ms * 1e-3) / 1e9);
+            cudaDeviceSynchronize();
+        }
+    }
     for (size_t c : {8ull << 20, 16ull << 20}) {
         run("copies_events", hin, hout, stage, 3, total, c, false, true, sh, sk, sd, 0);
         g_kernel_kind = 0;
