@@ -17,12 +17,19 @@
 //  * Round keys come by value in the kernel parameter (constant bank), so
 //    AddRoundKey folds into the 3-input LOP3 XOR trees for free.
 //  * Block-parallel kernel (CBC decrypt, ECB both ways): each warp streams a
-//    contiguous range of 16-byte blocks, one block per lane, 512-byte
-//    coalesced LDG.128/STG.128 per warp; the CBC predecessor C_{j-1} comes
-//    from the neighbouring lane by SHFL (lane 0: the previous unit's lane 31,
-//    or the IV at a page start).
+//    contiguous range of blocks; with even blocks-per-page (the default) each
+//    lane owns two consecutive blocks (1 KiB per warp step, coalesced
+//    LDG.256/STG.256), else one (512 B, LDG.128).  The CBC predecessor C_{j-1}
+//    comes from the neighbouring lane by one rotate-SHFL (lane 0: the previous
+//    unit's lane 31, or the IV at a page start); the next unit's load is in
+//    flight while the current unit's rounds run.
 //  * Chain kernel (CBC encrypt, serial within a page): one thread per page
-//    chain, pages balanced over a persistent grid of one CTA per SM.
+//    chain, pages balanced over a persistent grid of one CTA per SM; two
+//    blocks per 256-bit L1::no_allocate load/store (measured, profiles/r1_ldst).
+//  * Mixed-key kernel: same bodies, round keys per lane from a device
+//    snapshot of the key table.
+//  * Launches use programmatic dependent launch: the table fill runs before
+//    griddepcontrol.wait.
 //  * In-place safety (out == in): CTAs own whole pages; inside a CTA every
 //    warp snapshots the one predecessor block it needs from another warp
 //    BEFORE the CTA-wide barrier that precedes the first store.

@@ -467,8 +467,14 @@ int64_t nsk_post(uint32_t op, const void *in, void *out, const void *ivs, uint64
         // ordered after earlier work on `st`; later work on `st` waits for completion
         const CUdeviceptr bell = (CUdeviceptr)(uintptr_t)&g.nsk.ring_dev->doorbell[slot];
         const CUdeviceptr done = (CUdeviceptr)(uintptr_t)&g.nsk.ring_dev->done[slot];
-        if (g.write_value64((CUstream)st, bell, seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        if (g.write_value64((CUstream)st, bell, seq, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+            // the sequence number is spent: turn the slot into a no-op and ring it
+            // from the host so the NSK does not wait for it forever
+            vstore(&g.nsk.ring->req[slot].n_pages, 0);
+            std::atomic_thread_fence(std::memory_order_seq_cst);
+            vstore(&g.nsk.ring->doorbell[slot], seq);
             return KG_ECUDA;
+        }
         if (g.wait_value64((CUstream)st, done, seq, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) return KG_ECUDA;
     }
     return (int64_t)seq;
