@@ -43,11 +43,17 @@ namespace kg {
 namespace {
 
 constexpr int kThreads = 1024;
+#ifndef KG_POOL_DIV
+#define KG_POOL_DIV 16  // 1/KG_POOL_DIV of a CTA's pages form the tail-balancing pool
+#endif
 constexpr int kRegion = 65536;
 constexpr int kSmemEnc = 2 * kRegion;                       // Te0..Te3
 constexpr int kSmemDec = 2 * kRegion + 255 * 256 + 128;     // Td0..Td3 + Si (t = 0 slots only)
 
 __device__ BaseTables g_tables;
+#ifdef KG_CTA_STAMPS
+__device__ unsigned long long g_stamps[148 * 34];
+#endif
 
 __device__ __forceinline__ uint32_t rotl32(uint32_t v, int s) { return __funnelshift_l(v, v, s); }
 
@@ -313,32 +319,13 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
 // block is the previous lane's second block (one 4-word SHFL per 64 blocks),
 // that of its second block is its own first block.  A pair never straddles a
 // page (m even, ranges in whole pairs).
+
+// Stream the pairs [w0, w1) of one warp.  (n0, n1) holds the warp's first
+// unit (already loaded); carry = C of the block before w0 (if not a page start).
 template <bool DEC, bool CBC, class Cipher>
-__device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const uint64_t mp = a.m >> 1;  // pairs per page
-    uint64_t c0, c1;               // CTA range in pairs
-    if (a.in_place) {
-        c0 = part_start(a.n_pages, ncta, cta) * mp;
-        c1 = part_start(a.n_pages, ncta, cta + 1) * mp;
-    } else {
-        const uint64_t np = a.n_pages * mp;
-        c0 = part_start(np, ncta, cta);
-        c1 = part_start(np, ncta, cta + 1);
-    }
-    const uint64_t w0 = c0 + part_start(c1 - c0, nwarps, warp);
-    const uint64_t w1 = c0 + part_start(c1 - c0, nwarps, warp + 1);
-    uint64_t page = (w0 + lane) / mp;
-    uint32_t jp = (uint32_t)((w0 + lane) - page * mp);  // pair index in the page
-
-    uint4 carry = make_uint4(0, 0, 0, 0);
-    if (CBC && DEC) {
-        if (w0 < w1 && (w0 % mp) != 0) carry = a.in[2 * w0 - 1];
-    }
-    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-    if (w0 + lane < w1) ld256<false>(a.in + 2 * (w0 + lane), n0, n1);
-    __syncthreads();
-
+__device__ __forceinline__ void pair_stream(const Job &a, const Cipher &cph, uint64_t w0, uint64_t w1, uint64_t mp,
+                                            uint4 carry, uint64_t page, uint32_t jp, uint4 n0, uint4 n1) {
+    const uint32_t lane = threadIdx.x & 31;
     for (uint64_t u = w0; u < w1; u += 32) {
         const uint64_t q = u + lane;
         const bool act = q < w1;
@@ -369,6 +356,62 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
                 jp %= (uint32_t)mp;
             }
         }
+    }
+}
+
+// Tail balancing (large batches, pages of >= 1 KiB): the warp arbiter does not
+// progress the 32 warps of a CTA evenly -- with equal static shares the last
+// warp finished ~16 us (5%) after the first (profiles/r1_tail).  So only the
+// first 15/16 of a CTA's pages are split statically; the rest is a pool that
+// warps drain once their static share is done: 64-block units out of place
+// (the unit's CBC predecessor is re-read from `in`, which nobody writes),
+// whole pages in place (the IV starts each page, so no predecessor crosses
+// warps).
+template <bool DEC, bool CBC, class Cipher>
+__device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
+    __shared__ unsigned long long pool_next;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint64_t mp = a.m >> 1;  // pairs per page
+    const bool pool = mp >= 32 && a.n_pages >= 64ull * ncta;
+    uint64_t c0, c1, cmid;         // CTA range in pairs; the pool is [cmid, c1)
+    if (pool || a.in_place) {
+        const uint64_t P0 = part_start(a.n_pages, ncta, cta), P1 = part_start(a.n_pages, ncta, cta + 1);
+        c0 = P0 * mp;
+        c1 = P1 * mp;
+        cmid = pool ? (P1 - (P1 - P0) / KG_POOL_DIV) * mp : c1;
+        if (threadIdx.x == 0) pool_next = cmid;
+    } else {
+        const uint64_t np = a.n_pages * mp;
+        c0 = part_start(np, ncta, cta);
+        c1 = part_start(np, ncta, cta + 1);
+        cmid = c1;
+    }
+    const uint64_t w0 = c0 + part_start(cmid - c0, nwarps, warp);
+    const uint64_t w1 = c0 + part_start(cmid - c0, nwarps, warp + 1);
+    uint64_t page = (w0 + lane) / mp;
+    uint32_t jp = (uint32_t)((w0 + lane) - page * mp);  // pair index in the page
+
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    if (CBC && DEC) {
+        if (w0 < w1 && (w0 % mp) != 0) carry = a.in[2 * w0 - 1];
+    }
+    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+    if (w0 + lane < w1) ld256<false>(a.in + 2 * (w0 + lane), n0, n1);
+    __syncthreads();
+    pair_stream<DEC, CBC>(a, cph, w0, w1, mp, carry, page, jp, n0, n1);
+    if (!pool) return;
+    const uint64_t unit = a.in_place ? mp : 32;  // pairs per claim
+    for (;;) {
+        unsigned long long q0 = 0;
+        if (lane == 0) q0 = atomicAdd(&pool_next, (unsigned long long)unit);
+        q0 = __shfl_sync(0xffffffffu, q0, 0);
+        if (q0 >= c1) break;
+        const uint64_t pg = q0 / mp;
+        const uint32_t j0 = (uint32_t)(q0 - pg * mp);  // 0 in place; a multiple of 32 (< mp) otherwise
+        if (q0 + lane < c1) ld256<false>(a.in + 2 * (q0 + lane), n0, n1);
+        uint4 cr = make_uint4(0, 0, 0, 0);
+        if (CBC && DEC && j0 != 0) cr = a.in[2 * q0 - 1];  // out of place only
+        pair_stream<DEC, CBC>(a, cph, q0, q0 + unit, mp, cr, pg, j0 + lane, n0, n1);
     }
 }
 
@@ -422,13 +465,29 @@ __device__ __forceinline__ Job job_of(const LaunchArgs &a) {
 }
 
 // ---- launch-per-batch kernels -------------------------------------------------
+// 512 threads + a 1/16 pool measured best (profiles/r1_tail: 256..1024 threads,
+// pools of 1/4, 1/8, 1/16): 16 warps still saturate the LDS pipe and the
+// 89-register budget avoids the spills of the 64-register 1024-thread build.
+#ifndef KG_PAIR_TPB
+#define KG_PAIR_TPB 512
+#endif
+constexpr int kPairThreads = KG_PAIR_TPB;  // threads per CTA of the block-pair kernels
+
 template <int NR, int DIR, int MODE, bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant__ LaunchArgs a) {
+__global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
     constexpr bool DEC = (DIR == 1);
     constexpr bool CBC = (MODE == 0);
+#ifdef KG_CTA_STAMPS
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     fill_tables<DEC>(sm);
     pdl_prologue_done();
+#ifdef KG_CTA_STAMPS
+    unsigned long long t_filled;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_filled));
+#endif
     const uint32_t lb = lane_bytes();
     if (PAIR) {
         if (DEC) blockpair_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
@@ -437,6 +496,16 @@ __global__ void __launch_bounds__(kThreads, 1) kg_blockpar(const __grid_constant
         if (DEC) blockpar_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
         else blockpar_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
     }
+#ifdef KG_CTA_STAMPS
+    // per-warp finish time; per-CTA start / tables-filled times (diagnostics build only)
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    if ((threadIdx.x & 31) == 0) g_stamps[blockIdx.x * 34 + 2 + (threadIdx.x >> 5)] = t_end;
+    if (threadIdx.x == 0) {
+        g_stamps[blockIdx.x * 34 + 0] = t_start;
+        g_stamps[blockIdx.x * 34 + 1] = t_filled;
+    }
+#endif
 }
 
 template <int NR, bool WIDE>
@@ -573,10 +642,11 @@ cudaError_t init_nr() {
 
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaStream_t st, const Args &...args) {
+cudaError_t launch_pdl_tpb(void (*kernel)(KArgs...), unsigned grid, unsigned tpb, int smem, cudaStream_t st,
+                           const Args &...args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(tpb);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -589,6 +659,11 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaSt
     }();
     cfg.numAttrs = use_pdl;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaStream_t st, const Args &...args) {
+    return launch_pdl_tpb(kernel, grid, kThreads, smem, st, args...);
 }
 
 template <int NR>
@@ -609,9 +684,9 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
         return (e && *e == '0') ? 0 : 1;
     }();
     if (pair_ok && (a.m & 1) == 0) {
-        if (dir == 1 && mode == 0) return launch_pdl(kg_blockpar<NR, 1, 0, true>, grid, kSmemDec, st, a);
-        if (dir == 1) return launch_pdl(kg_blockpar<NR, 1, 1, true>, grid, kSmemDec, st, a);
-        return launch_pdl(kg_blockpar<NR, 0, 1, true>, grid, kSmemEnc, st, a);
+        if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_blockpar<NR, 1, 0, true>, grid, kPairThreads, kSmemDec, st, a);
+        if (dir == 1) return launch_pdl_tpb(kg_blockpar<NR, 1, 1, true>, grid, kPairThreads, kSmemDec, st, a);
+        return launch_pdl_tpb(kg_blockpar<NR, 0, 1, true>, grid, kPairThreads, kSmemEnc, st, a);
     }
     if (dir == 1 && mode == 0) return launch_pdl(kg_blockpar<NR, 1, 0, false>, grid, kSmemDec, st, a);
     if (dir == 1) return launch_pdl(kg_blockpar<NR, 1, 1, false>, grid, kSmemDec, st, a);
