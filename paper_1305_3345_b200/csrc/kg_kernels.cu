@@ -511,10 +511,27 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
 template <int NR, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
+#ifdef KG_CTA_STAMPS
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     fill_tables<false>(sm);
     pdl_prologue_done();
     __syncthreads();
+#ifdef KG_CTA_STAMPS
+    unsigned long long t_filled;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_filled));
+#endif
     cbc_enc_body<WIDE>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
+#ifdef KG_CTA_STAMPS
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    if ((threadIdx.x & 31) == 0) g_stamps[blockIdx.x * 34 + 2 + (threadIdx.x >> 5)] = t_end;
+    if (threadIdx.x == 0) {
+        g_stamps[blockIdx.x * 34 + 0] = t_start;
+        g_stamps[blockIdx.x * 34 + 1] = t_filled;
+    }
+#endif
 }
 
 // ---- mixed-key batches -------------------------------------------------------
@@ -673,8 +690,7 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
         const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
         if ((a.m & 1) == 0) return launch_pdl(kg_cbc_enc<NR, true>, grid, kSmemEnc, st, a);
         return launch_pdl(kg_cbc_enc<NR, false>, grid, kSmemEnc, st, a);
-    }
-    uint64_t want = (nb + 255) / 256;
+    }    uint64_t want = (nb + 255) / 256;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
     if (want < 1) want = 1;

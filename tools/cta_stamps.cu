@@ -7,14 +7,15 @@
 
 #include <stdio.h>
 
-int main() {
+int main(int argc, char **argv) {
+    const bool enc = argc > 1 && argv[1][0] == 'e';  // "enc": C3 AES-256-CBC encrypt 1 GiB
     kg::BaseTables t;
     kg::build_base_tables(&t);
     if (kg::kernels_init(t) != cudaSuccess) return 1;
-    uint8_t key[16] = {1, 2, 3, 4};
-    kg::RoundKeys enc, dec;
-    kg::expand_key(key, 16, &enc, &dec);
-    const uint64_t n = 65536, pb = 4096;
+    uint8_t key[32] = {1, 2, 3, 4};
+    kg::RoundKeys enc_k, dec_k;
+    kg::expand_key(key, enc ? 32 : 16, &enc_k, &dec_k);
+    const uint64_t n = enc ? 262144 : 65536, pb = 4096;
     uint8_t *in, *out, *iv;
     cudaMalloc(&in, n * pb);
     cudaMalloc(&out, n * pb);
@@ -27,8 +28,8 @@ int main() {
     a.n_pages = n;
     a.m = pb / 16;
     a.in_place = 0;
-    a.rk = dec;
-    for (int rep = 0; rep < 5; rep++) kg::launch_pages(1, 0, 10, a, 148, 0);
+    a.rk = enc ? enc_k : dec_k;
+    for (int rep = 0; rep < 5; rep++) kg::launch_pages(enc ? 0 : 1, 0, enc ? 14 : 10, a, 148, 0);
     cudaDeviceSynchronize();
     static unsigned long long h[148 * 34];
     cudaMemcpyFromSymbol(h, kg::g_stamps, sizeof h);
