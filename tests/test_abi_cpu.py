@@ -67,3 +67,24 @@ def test_kernel_image_is_sm100a():
         pytest.skip("cuobjdump not available")
     out = subprocess.run([exe, "--list-elf", kg.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_header_is_plain_c_and_cxx(tmp_path):
+    """include/kg.h compiles as C99 and as C++ (no torch or CUDA types)."""
+    import subprocess
+    src = tmp_path / "t.c"
+    src.write_text('#include "kg.h"\nint main(void){ return kg_strerror(KG_OK) == 0; }\n')
+    inc = os.path.join(ROOT, "include")
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-pedantic", "-fsyntax-only", "-I", inc, str(src)])
+    subprocess.check_call(["g++", "-std=c++11", "-Wall", "-Werror", "-fsyntax-only", "-x", "c++", "-I", inc, str(src)])
+
+
+def test_example_links_against_the_library(tmp_path):
+    import subprocess
+    import paper_1305_3345_b200 as kg
+    exe = tmp_path / "kgpu_crypt"
+    subprocess.check_call(["gcc", "-std=c99", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "kgpu_crypt.c"), "-L", os.path.dirname(kg.LIB_PATH),
+                           "-lkgpu", f"-Wl,-rpath,{os.path.dirname(kg.LIB_PATH)}", "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 2 and "usage" in out.stderr
