@@ -38,7 +38,19 @@ build/latency: tools/latency.cu include/kg.h $(LIB) | build
 build/kgpu_crypt: examples/kgpu_crypt.c include/kg.h $(LIB) | build
 	gcc -std=c99 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lkgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
+# diagnostics (not part of `all`): copy-engine overlap, per-CTA stamps, bitsliced round
+tools: build/copy_overlap build/cta_stamps build/bitslice_bench
+
+build/copy_overlap: tools/copy_overlap.cu | build
+	$(NVCC) -O2 $(ARCH) -o $@ $<
+
+build/cta_stamps: tools/cta_stamps.cu $(CSRC)/kg_kernels.cu $(CSRC)/kg_tables.cpp $(wildcard $(CSRC)/*.cuh) | build
+	$(NVCC) -O3 -std=c++17 $(ARCH) -o $@ $< $(CSRC)/kg_tables.cpp
+
+build/bitslice_bench: tools/bitslice_bench.cu tools/kg_sbox_bs.cuh | build
+	$(NVCC) -O3 -std=c++17 $(ARCH) -o $@ $<
+
 clean:
 	rm -rf build $(LIB) oracle/libkgo.so
 
-.PHONY: all clean
+.PHONY: all clean tools
