@@ -46,7 +46,12 @@ WORKLOADS = {
     "c2": (65536, 16, 1, False, "C2 eCryptfs-shaped read: AES-128-CBC decrypt, 65,536 x 4 KiB pages (256 MiB) per GPU, HBM-resident, out-of-place"),
     "c3": (262144, 32, 0, False, "C3 eCryptfs-shaped write: AES-256-CBC encrypt (page-parallel chains), 262,144 x 4 KiB pages (1 GiB) per GPU, HBM-resident"),
     "c5": (16777216, 16, 1, True, "C5: AES-128-CBC decrypt of 64 GiB (16,777,216 x 4 KiB pages) page-range sharded over the ranks, HBM-resident, in place"),
+    # not BASELINE configs: the paper's own ECB mode (row f1) and mixed-key batches
+    "ecb_dec": (65536, 16, 1, False, "AES-128-ECB decrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
+    "ecb_enc": (65536, 16, 0, False, "AES-128-ECB encrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
+    "c2_keyed": (65536, 16, 1, False, "C2 with a key id per page (8 AES-128 keys, uniform), HBM, out-of-place"),
 }
+MODE_OF = {"ecb_dec": 1, "ecb_enc": 1}
 SM_COUNT = 148
 LDS_LANES_PER_CLK = 32      # lane-lookups/clk/SM (B300_MICROARCH.md "smem crossbar 128/N B/cyc/SM"; tools/pipes.cu measures it)
 
@@ -259,6 +264,11 @@ def run_ours(args):
     n = hi - lo
     key = synth.make_key(key_bytes)
     kg.set_key(0, key)
+    mode = MODE_OF.get(args.workload, kg.MODE_CBC)
+    keyed = args.workload == "c2_keyed"
+    if keyed:
+        for i in range(8):
+            kg.set_key(i, synth.make_key(key_bytes, seed=synth.KEY_SEED + 100 + i))
     stream = torch.cuda.current_stream()
 
     # inputs: seeded pages (C2/C3: the full batch; C5: periodic M-page pattern)
@@ -280,10 +290,16 @@ def run_ours(args):
         x = torch.from_numpy(synth.make_pages(n, PB, first_page=lo)).cuda()
         ivs = torch.from_numpy(synth.make_ivs(n, first_page=lo)).cuda()
     out = x if in_place else torch.empty_like(x)
+    key_ids = None
+    if keyed:
+        key_ids = torch.from_numpy((synth.stream_bytes(synth.KEY_SEED + 7, 2 * n).view(np.uint16) % 8)
+                                   .astype(np.int16)).cuda()
     torch.cuda.synchronize()
 
     def step():
-        return kg.submit_pages(direction, kg.MODE_CBC, x, out, n, PB, ivs, 0, stream)
+        if keyed:
+            return kg.submit_pages_keyed(direction, mode, x, out, n, PB, ivs, key_ids, key_bytes, stream)
+        return kg.submit_pages(direction, mode, x, out, n, PB, ivs if mode == kg.MODE_CBC else None, 0, stream)
 
     # warm-up (also loads the module lazily)
     for _ in range(args.warmup):
@@ -324,7 +340,7 @@ def run_ours(args):
 
     # secondary: e2e through the C ABI with pinned HOST buffers (H2D + compute + D2H timed)
     e2e = None
-    if args.workload != "c5" and not args.no_e2e:
+    if args.workload in ("c2", "c3") and not args.no_e2e:
         e_steps = max(1, min(args.steps, args.e2e_steps))
         hx = torch.empty(n * PB, dtype=torch.uint8).pin_memory()
         hx.copy_(x.cpu())
@@ -370,7 +386,8 @@ def run_ours(args):
         "frac_at_measured_clock": (achieved / compute_peak_gbs(key_bytes, clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
         "hbm_payload_peak": peaks["hbm_gbs"] / (2 + 16.0 / PB),
         "hbm_frac": achieved / (peaks["hbm_gbs"] / (2 + 16.0 / PB)),
-        "kernel": "kg_blockpar<10,DEC,CBC>" if direction == 1 else f"kg_cbc_enc<{nr_of(key_bytes)}>",
+        "kernel": ("kg_keyed" if keyed else "kg_blockpar" if (direction == 1 or mode == kg.MODE_ECB)
+                   else "kg_cbc_enc") + f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>",
         "algorithmic_bytes_per_launch": bytes_step,
     }
     line = {
@@ -378,7 +395,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": desc, "n_pages_per_gpu": n, "page_bytes": PB, "key_bits": 8 * key_bytes,
-                   "dir": "decrypt" if direction else "encrypt", "mode": "cbc", "residency": "hbm",
+                   "dir": "decrypt" if direction else "encrypt", "mode": "ecb" if mode else "cbc", "residency": "hbm",
                    "l2": f"no flush: each step reads {bytes_step / 2**20:.0f} MiB and writes "
                          f"{bytes_step / 2**20:.0f} MiB, > 126 MB L2",
                    "parallelism": f"page-range x{world}" if world > 1 else "1 GPU"},
