@@ -215,11 +215,12 @@ KG_API int kg_nsk_stop(void);
 KG_API int kg_nsk_dispatch(uint64_t max_bytes, uint64_t *chosen);
 
 /* Pinned host allocations for batches (row f4; "allocate memory in the pinned
- * region ... to save an extra copy"): `bytes` rounded up to
- * 2 MiB, first-touched by threads bound to the CPUs local to the context's
- * GPU (sysfs local_cpulist: NUMA-local pages without libnuma), then pinned
- * and mapped (cudaHostRegister).  Usable as in/out/ivs of kg_submit_pages
- * (staged or zero-copy).  Returns NULL if not initialised or on failure.
+ * region ... to save an extra copy"): pinned and mapped
+ * memory allocated from a thread bound to the CPUs local to the context's GPU
+ * (sysfs local_cpulist), so the pages land on the GPU's NUMA node without
+ * libnuma (cudaHostAlloc; KG_PINNED_MODE=register instead first-touches an
+ * mmap region on those CPUs and registers it).  Usable as in/out/ivs of
+ * kg_submit_pages (staged or zero-copy).  NULL if not initialised or on failure.
  * kg_free_pinned: KG_EINVAL if `p` did not come from kg_alloc_pinned. */
 KG_API void *kg_alloc_pinned(uint64_t bytes);
 KG_API int kg_free_pinned(void *p);

@@ -651,13 +651,38 @@ bool local_cpus(int device, cpu_set_t *set) {
 void *kg_alloc_pinned(uint64_t bytes) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g.up || bytes == 0) return nullptr;
+    cpu_set_t local;
+    const bool have_local = local_cpus(g.device, &local);
+    static const bool use_register = [] {
+        const char *e = getenv("KG_PINNED_MODE");
+        return e && strcmp(e, "register") == 0;
+    }();
+    if (!use_register) {
+        // cudaHostAlloc from a thread bound to the GPU-local CPUs: the driver
+        // touches the pages there, so they land on the GPU's NUMA node, and its
+        // allocation DMAs faster than mmap + cudaHostRegister here
+        // (profiles/r1_pinned: 49 vs 38 GB/s per direction duplex).
+        void *p = nullptr;
+        cudaError_t e = cudaSuccess;
+        const int dev = g.device;
+        std::thread t([&] {
+            if (have_local) sched_setaffinity(0, sizeof local, &local);
+            cudaSetDevice(dev);
+            e = cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+        });
+        t.join();
+        if (e != cudaSuccess || !p) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        g_pinned[p] = 0;  // 0 = cudaHostAlloc'd
+        return p;
+    }
     const uint64_t align = 2ull << 20;
     const uint64_t len = (bytes + align - 1) / align * align;
     void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
     if (p == MAP_FAILED) return nullptr;
     madvise(p, len, MADV_HUGEPAGE);
-    cpu_set_t local;
-    const bool have_local = local_cpus(g.device, &local);
     unsigned nthr = have_local ? (unsigned)CPU_COUNT(&local) : std::thread::hardware_concurrency();
     if (nthr < 1) nthr = 1;
     if (nthr > 16) nthr = 16;
@@ -685,9 +710,13 @@ int kg_free_pinned(void *p) {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_pinned.find(p);
     if (it == g_pinned.end()) return KG_EINVAL;
-    cudaHostUnregister(p);
+    if (it->second == 0) {
+        cudaFreeHost(p);
+    } else {
+        cudaHostUnregister(p);
+        munmap(p, it->second);
+    }
     cudaGetLastError();
-    munmap(p, it->second);
     g_pinned.erase(it);
     return KG_OK;
 }
