@@ -20,7 +20,7 @@ def expected(direction, mode, keys, ids, data, n, pb, ivs):
 
 @pytest.mark.parametrize("key_bytes", [16, 24, 32])
 @pytest.mark.parametrize("direction,mode", [(0, 0), (1, 0), (0, 1), (1, 1)])
-@pytest.mark.parametrize("n,pb", [(37, 4096), (300, 512), (5, 48), (300, 256), (9000, 4096)])
+@pytest.mark.parametrize("n,pb", [(37, 4096), (300, 512), (5, 48), (300, 256), (1500, 4096)])
 def test_keyed_parity(key_bytes, direction, mode, n, pb):
     kg, torch = kg_ready()
     key_set = [10, 11, 200, 255, 0]
