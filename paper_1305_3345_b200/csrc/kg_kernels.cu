@@ -406,12 +406,14 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
         if (lane == 0) q0 = atomicAdd(&pool_next, (unsigned long long)unit);
         q0 = __shfl_sync(0xffffffffu, q0, 0);
         if (q0 >= c1) break;
-        const uint64_t pg = q0 / mp;
-        const uint32_t j0 = (uint32_t)(q0 - pg * mp);  // 0 in place; a multiple of 32 (< mp) otherwise
+        // per-lane page / pair index (a 32-pair unit may cross a page boundary
+        // when mp is not a multiple of 32)
+        const uint64_t pg = (q0 + lane) / mp;
+        const uint32_t jl = (uint32_t)(q0 + lane - pg * mp);
         if (q0 + lane < c1) ld256<false>(a.in + 2 * (q0 + lane), n0, n1);
         uint4 cr = make_uint4(0, 0, 0, 0);
-        if (CBC && DEC && j0 != 0) cr = a.in[2 * q0 - 1];  // out of place only
-        pair_stream<DEC, CBC>(a, cph, q0, q0 + unit, mp, cr, pg, j0 + lane, n0, n1);
+        if (CBC && DEC && q0 % mp != 0) cr = a.in[2 * q0 - 1];  // out of place only (in place: q0 is a page start)
+        pair_stream<DEC, CBC>(a, cph, q0, q0 + unit, mp, cr, pg, jl, n0, n1);
     }
 }
 

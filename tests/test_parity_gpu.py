@@ -187,3 +187,21 @@ def test_staged_batches_back_to_back():
     finally:
         kg.set_pipeline(16 << 20, 3)
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
+
+
+@pytest.mark.parametrize("pb", [1056, 4096, 2080])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_tail_pool_large_batches(pb, inplace):
+    """Batches large enough for the block-pair kernel's tail-balancing pool
+    (>= 64 pages per CTA), incl. pair counts per page that are not multiples of
+    32 (pool units then straddle page boundaries)."""
+    n = 64 * 148 + 37
+    key = synth.make_key(16, seed=pb + inplace)
+    data = synth.make_pages(n, pb, seed=pb)
+    ivs = synth.make_ivs(n, seed=pb + 1)
+    exp = oracle_pages(1, 0, key, data, n, pb, ivs)
+    got = gpu_pages(1, 0, key, data, n, pb, ivs, where="device", inplace=inplace)
+    assert first_mismatch(got, exp) is None
+    exp_e = oracle_pages(1, 1, key, data, n, pb, None)
+    got_e = gpu_pages(1, 1, key, data, n, pb, None, where="device", inplace=inplace)
+    assert first_mismatch(got_e, exp_e) is None
