@@ -413,7 +413,8 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
         if (q0 + lane < c1) ld256<false>(a.in + 2 * (q0 + lane), n0, n1);
         uint4 cr = make_uint4(0, 0, 0, 0);
         if (CBC && DEC && q0 % mp != 0) cr = a.in[2 * q0 - 1];  // out of place only (in place: q0 is a page start)
-        pair_stream<DEC, CBC>(a, cph, q0, q0 + unit, mp, cr, pg, jl, n0, n1);
+        const uint64_t q1 = q0 + unit < c1 ? q0 + unit : c1;  // the last unit may be partial
+        pair_stream<DEC, CBC>(a, cph, q0, q1, mp, cr, pg, jl, n0, n1);
     }
 }
 
