@@ -316,17 +316,22 @@ def run_ours(args):
         t_wall0 = time.perf_counter()
         tickets = []
         for i in range(args.steps):
-            starts[i].record(stream)
+            if args.step_events or i == 0:
+                starts[i].record(stream)
             tickets.append(step())
-            ends[i].record(stream)
+            if args.step_events or i == args.steps - 1:
+                ends[i].record(stream)
         for t in tickets:
             kg.wait(t)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     launches = kg.launch_count() - l0
     elapsed = starts[0].elapsed_time(ends[-1]) / 1e3                   # s, device-timed
-    per_launch = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
-    avg_launch = sum(per_launch) / len(per_launch)
+    if args.step_events:
+        per_launch = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
+        avg_launch = sum(per_launch) / len(per_launch)
+    else:
+        avg_launch = elapsed / args.steps  # one launch per step, back to back on one stream
     if dist:
         t = torch.tensor([elapsed, avg_launch], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -439,6 +444,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--step-events", action="store_true",
+                    help="record a CUDA event pair around every step (serialises programmatic dependent launch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
