@@ -162,3 +162,46 @@ def test_nsk_size_dispatch(nsk):
     ivs = synth.make_ivs(n, seed=78)
     exp = oracle_pages(0, 0, key, data, n, 4096, ivs)
     assert first_mismatch(run(kg, torch, 0, 0, key, data, n, 4096, ivs, "pinned"), exp) is None
+
+
+def test_nsk_multithreaded_soak(nsk):
+    """Several host threads post to the NSK concurrently (ring wrap-around,
+    completion words, waiter accounting); every ticket completes once and the
+    outputs are right."""
+    import threading
+    kg, torch = nsk
+    kg.nsk_start(8, kg.NSK_DIRECT, 5000)
+    n, pb = 16, 4096
+    key = synth.make_key(16, seed=77)
+    kg.set_key(3, key)
+    data = synth.make_pages(n, pb, seed=78)
+    ivs = synth.make_ivs(n, seed=79)
+    exp = oracle_pages(1, 0, key, data, n, pb, ivs)
+    src = torch.from_numpy(data).cuda()
+    iv = torch.from_numpy(ivs).cuda()
+    torch.cuda.current_stream().synchronize()
+    errors, seen = [], []
+    lock = threading.Lock()
+
+    def worker(tid):
+        try:
+            outs = [torch.empty_like(src) for _ in range(3)]
+            torch.cuda.current_stream().synchronize()
+            for i in range(300):
+                o = outs[i % 3]
+                t = kg.submit_pages(1, 0, src, o, n, pb, iv, 3)
+                with lock:
+                    seen.append(t)
+                kg.wait(t)
+                if i % 71 == 0 and not np.array_equal(o.cpu().numpy(), exp):
+                    errors.append((tid, i))
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ths = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors[:5]
+    assert len(seen) == len(set(seen)) == 1200
