@@ -39,7 +39,7 @@ build/kgpu_crypt: examples/kgpu_crypt.c include/kg.h $(LIB) | build
 	gcc -std=c99 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lkgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 # diagnostics (not part of `all`): copy-engine overlap, per-CTA stamps, bitsliced round
-tools: build/copy_overlap build/cta_stamps build/bitslice_bench
+tools: build/copy_overlap build/cta_stamps build/bitslice_bench build/soak_tsan
 
 build/copy_overlap: tools/copy_overlap.cu | build
 	$(NVCC) -O2 $(ARCH) -o $@ $<
@@ -49,6 +49,13 @@ build/cta_stamps: tools/cta_stamps.cu $(CSRC)/kg_kernels.cu $(CSRC)/kg_tables.cp
 
 build/bitslice_bench: tools/bitslice_bench.cu tools/kg_sbox_bs.cuh | build
 	$(NVCC) -O3 -std=c++17 $(ARCH) -o $@ $<
+
+# host runtime under ThreadSanitizer (kernels unchanged; kg_runtime.cpp + kg_tables.cpp instrumented)
+build/soak_tsan: tools/soak_tsan.cpp $(CSRC)/kg_runtime.cpp $(CSRC)/kg_tables.cpp build/kg_kernels.o | build
+	g++ -std=c++17 -O1 -g -fsanitize=thread -Iinclude -I/usr/local/cuda/include -c $(CSRC)/kg_runtime.cpp -o build/kg_runtime_tsan.o
+	g++ -std=c++17 -O1 -g -fsanitize=thread -I/usr/local/cuda/include -c $(CSRC)/kg_tables.cpp -o build/kg_tables_tsan.o
+	$(NVCC) $(ARCH) -o $@ tools/soak_tsan.cpp build/kg_runtime_tsan.o build/kg_tables_tsan.o build/kg_kernels.o \
+	  -Iinclude -Xcompiler -fsanitize=thread -ltsan -lpthread
 
 clean:
 	rm -rf build $(LIB) oracle/libkgo.so
