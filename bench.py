@@ -50,7 +50,9 @@ WORKLOADS = {
     "ecb_dec": (65536, 16, 1, False, "AES-128-ECB decrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
     "ecb_enc": (65536, 16, 0, False, "AES-128-ECB encrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
     "c2_keyed": (65536, 16, 1, False, "C2 with a key id per page (8 AES-128 keys, uniform), HBM, out-of-place"),
+    "c3_keyed": (262144, 32, 0, False, "C3 with a key id per page (8 AES-256 keys, uniform), HBM, out-of-place"),
 }
+KEYED = ("c2_keyed", "c3_keyed")
 MODE_OF = {"ecb_dec": 1, "ecb_enc": 1}
 SM_COUNT = 148
 LDS_LANES_PER_CLK = 32      # lane-lookups/clk/SM (B300_MICROARCH.md "smem crossbar 128/N B/cyc/SM"; tools/pipes.cu measures it)
@@ -265,7 +267,7 @@ def run_ours(args):
     key = synth.make_key(key_bytes)
     kg.set_key(0, key)
     mode = MODE_OF.get(args.workload, kg.MODE_CBC)
-    keyed = args.workload == "c2_keyed"
+    keyed = args.workload in KEYED
     if keyed:
         for i in range(8):
             kg.set_key(i, synth.make_key(key_bytes, seed=synth.KEY_SEED + 100 + i))
@@ -405,8 +407,8 @@ def run_ours(args):
         "frac_at_measured_clock": (achieved / compute_peak_gbs(key_bytes, clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
         "hbm_payload_peak": peaks["hbm_gbs"] / (2 + 16.0 / PB),
         "hbm_frac": achieved / (peaks["hbm_gbs"] / (2 + 16.0 / PB)),
-        "kernel": ("kg_keyed" if keyed else "kg_blockpar" if (direction == 1 or mode == kg.MODE_ECB)
-                   else "kg_cbc_enc") + f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>",
+        "kernel": (("kg_keyed_chain" if (direction == 0 and mode == kg.MODE_CBC) else "kg_keyed_pair") if keyed
+                   else "kg_blockpar" if (direction == 1 or mode == kg.MODE_ECB) else "kg_cbc_enc") + f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>",
         "algorithmic_bytes_per_launch": bytes_step,
     }
     line = {

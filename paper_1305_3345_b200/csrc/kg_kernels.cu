@@ -618,6 +618,159 @@ struct KeyedPolicy {
     }
 };
 
+// Generic round functions over a key accessor key(r) -> uint4 (round key r).
+template <int NR, class KeyAt>
+__device__ __forceinline__ uint4 enc_rounds_k(const char *sm, uint32_t lb, uint4 s, const KeyAt &key) {
+    uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+        const uint4 kr = key(r);
+        const uint32_t t0 = T<0>(sm, s0, lb) ^ T<1>(sm, s1, lb) ^ T<2>(sm, s2, lb) ^ T<3>(sm, s3, lb) ^ kr.x;
+        const uint32_t t1 = T<0>(sm, s1, lb) ^ T<1>(sm, s2, lb) ^ T<2>(sm, s3, lb) ^ T<3>(sm, s0, lb) ^ kr.y;
+        const uint32_t t2 = T<0>(sm, s2, lb) ^ T<1>(sm, s3, lb) ^ T<2>(sm, s0, lb) ^ T<3>(sm, s1, lb) ^ kr.z;
+        const uint32_t t3 = T<0>(sm, s3, lb) ^ T<1>(sm, s0, lb) ^ T<2>(sm, s1, lb) ^ T<3>(sm, s2, lb) ^ kr.w;
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    const uint4 kl = key(NR);
+    uint4 o;
+#define KG_ENC_LAST(dst, a, b, c, d, kw)                                                                  \
+    dst = __byte_perm(__byte_perm(T<0>(sm, a, lb), T<1>(sm, b, lb), 0x0061u),                             \
+                      __byte_perm(T<2>(sm, c, lb), T<3>(sm, d, lb), 0x4300u), 0x7610u) ^ kw;
+    KG_ENC_LAST(o.x, s0, s1, s2, s3, kl.x)
+    KG_ENC_LAST(o.y, s1, s2, s3, s0, kl.y)
+    KG_ENC_LAST(o.z, s2, s3, s0, s1, kl.z)
+    KG_ENC_LAST(o.w, s3, s0, s1, s2, kl.w)
+#undef KG_ENC_LAST
+    return o;
+}
+
+template <int NR, class KeyAt>
+__device__ __forceinline__ uint4 dec_rounds_k(const char *sm, uint32_t lb, uint4 s, const KeyAt &key) {
+    uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+        const uint4 kr = key(r);
+        const uint32_t t0 = T<0>(sm, s0, lb) ^ T<1>(sm, s3, lb) ^ T<2>(sm, s2, lb) ^ T<3>(sm, s1, lb) ^ kr.x;
+        const uint32_t t1 = T<0>(sm, s1, lb) ^ T<1>(sm, s0, lb) ^ T<2>(sm, s3, lb) ^ T<3>(sm, s2, lb) ^ kr.y;
+        const uint32_t t2 = T<0>(sm, s2, lb) ^ T<1>(sm, s1, lb) ^ T<2>(sm, s0, lb) ^ T<3>(sm, s3, lb) ^ kr.z;
+        const uint32_t t3 = T<0>(sm, s3, lb) ^ T<1>(sm, s2, lb) ^ T<2>(sm, s1, lb) ^ T<3>(sm, s0, lb) ^ kr.w;
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    const uint4 kl = key(NR);
+    uint4 o;
+#define KG_DEC_LAST(dst, a, b, c, d, kw)                                                                  \
+    dst = __byte_perm(__byte_perm(IS<0>(sm, a, lb), IS<1>(sm, b, lb), 0x0040u),                           \
+                      __byte_perm(IS<2>(sm, c, lb), IS<3>(sm, d, lb), 0x4000u), 0x7610u) ^ kw;
+    KG_DEC_LAST(o.x, s0, s3, s2, s1, kl.x)
+    KG_DEC_LAST(o.y, s1, s0, s3, s2, kl.y)
+    KG_DEC_LAST(o.z, s2, s1, s0, s3, kl.z)
+    KG_DEC_LAST(o.w, s3, s2, s1, s0, kl.w)
+#undef KG_DEC_LAST
+    return o;
+}
+
+// The launch direction's schedules of a key-table snapshot in the constant
+// bank (kg_load_const_keys copies them in stream order before the launch):
+// a warp whose lanes share a page reads its round key with one uniform LDC
+// per round from the constant cache, which does not occupy the L1 data pipe
+// the table lookups saturate.
+__constant__ uint4 c_keys[kMaxKeys][15];
+__constant__ uint8_t c_nr[kMaxKeys];
+
+template <int NR, bool DEC>
+struct ConstKeyPolicy {
+    const char *sm;
+    uint32_t lb;
+    const uint16_t *ids;
+    uint32_t *status;
+    uint64_t n_pages;
+    struct L {
+        uint32_t id;
+    };
+    struct KeyAt {
+        uint32_t id;
+        __device__ __forceinline__ uint4 operator()(int r) const { return c_keys[id][r]; }
+    };
+    __device__ __forceinline__ L lane(uint64_t page) const {
+        if (page >= n_pages) page = n_pages - 1;  // inactive tail lanes
+        uint32_t id = __ldg(ids + page);
+        if (id >= (uint32_t)kMaxKeys || c_nr[id] != NR) {
+            atomicOr(status, 1u);
+            id = 0;
+        }
+        return L{id};
+    }
+    __device__ __forceinline__ uint4 first(L l, uint4 x) const { return xor4(x, c_keys[l.id][0]); }
+    __device__ __forceinline__ uint4 rounds(L l, uint4 s) const {
+        return DEC ? dec_rounds_k<NR>(sm, lb, s, KeyAt{l.id}) : enc_rounds_k<NR>(sm, lb, s, KeyAt{l.id});
+    }
+};
+
+// Chain (CBC-encrypt) threads each own a page, so the lanes of a warp
+// generally hold different keys: the page's whole schedule is loaded into
+// registers once per page (Nr+1 16-byte loads per 4 KiB chain).
+template <int NR>
+struct RegKeyPolicy {
+    const char *sm;
+    uint32_t lb;
+    const uint4 (*tab)[15];
+    const uint8_t *nr;
+    const uint16_t *ids;
+    uint32_t *status;
+    uint64_t n_pages;
+    struct L {
+        uint4 k[NR + 1];
+    };
+    struct KeyAt {
+        const L &l;
+        __device__ __forceinline__ uint4 operator()(int r) const { return l.k[r]; }
+    };
+    __device__ __forceinline__ L lane(uint64_t page) const {
+        uint32_t id = __ldg(ids + page);
+        if (id >= (uint32_t)kMaxKeys || nr[id] != NR) {
+            atomicOr(status, 1u);
+            id = 0;
+        }
+        L l;
+#pragma unroll
+        for (int r = 0; r <= NR; ++r) l.k[r] = __ldg(&tab[id][r]);
+        return l;
+    }
+    __device__ __forceinline__ uint4 first(const L &l, uint4 x) const { return xor4(x, l.k[0]); }
+    __device__ __forceinline__ uint4 rounds(const L &l, uint4 s) const { return enc_rounds_k<NR>(sm, lb, s, KeyAt{l}); }
+};
+
+// Mixed-key block-pair kernel (m even): CBC decrypt, ECB both ways.
+// CONSTK: round keys from the constant bank (ConstKeyPolicy), else per-lane
+// __ldg from the device snapshot (KeyedPolicy).
+template <int NR, int DIR, int MODE, bool CONSTK>
+__global__ void __launch_bounds__(kPairThreads, 1) kg_keyed_pair(const __grid_constant__ LaunchArgs a, KeyedArgs k) {
+    extern __shared__ __align__(16) char sm[];
+    constexpr bool DEC = (DIR == 1);
+    constexpr bool CBC = (MODE == 0);
+    fill_tables<DEC>(sm);
+    pdl_prologue_done();
+    const uint32_t lb = lane_bytes();
+    if (CONSTK) {
+        const ConstKeyPolicy<NR, DEC> pol{sm, lb, k.key_ids, k.status, a.n_pages};
+        blockpair_body<DEC, CBC>(job_of(a), pol, blockIdx.x, gridDim.x);
+    } else {
+        const KeyedPolicy<NR, DEC> pol{sm, lb, DEC ? k.tab->dec : k.tab->enc, k.tab->nr, k.key_ids, k.status, a.n_pages};
+        blockpair_body<DEC, CBC>(job_of(a), pol, blockIdx.x, gridDim.x);
+    }
+}
+
+// Mixed-key CBC encrypt: one chain per thread, the page's keys in registers.
+template <int NR, bool WIDE>
+__global__ void __launch_bounds__(kPairThreads, 1) kg_keyed_chain(const __grid_constant__ LaunchArgs a, KeyedArgs k) {
+    extern __shared__ __align__(16) char sm[];
+    fill_tables<false>(sm);
+    pdl_prologue_done();
+    __syncthreads();
+    const RegKeyPolicy<NR> pol{sm, lane_bytes(), k.tab->enc, k.tab->nr, k.key_ids, k.status, a.n_pages};
+    cbc_enc_body<WIDE>(job_of(a), pol, blockIdx.x, gridDim.x);
+}
+
 template <int NR, int DIR, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) kg_keyed(const __grid_constant__ LaunchArgs a, KeyedArgs k) {
     extern __shared__ __align__(16) char sm[];
@@ -657,6 +810,14 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_keyed<NR, 1, 1>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed<NR, 0, 1>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed<NR, 0, 0>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 1, 0, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 1, 1, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 0, 1, true>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 1, 0, false>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 1, 1, false>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 0, 1, false>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_chain<NR, true>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_chain<NR, false>, kSmemEnc)) != cudaSuccess) return e;
     return cudaSuccess;
 }
 
@@ -712,14 +873,41 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
     return launch_pdl(kg_blockpar<NR, 0, 1, false>, grid, kSmemEnc, st, a);
 }
 
+// KG_KEYED (A/B switch): 0 = one block per lane, 1024 threads, per-lane __ldg
+// keys (kg_keyed); 1 = block pairs + per-lane __ldg keys; 2 (default) = block
+// pairs + constant-bank keys; CBC encrypt: register keys (1, 2) or kg_keyed (0).
+int keyed_variant() {
+    static const int v = [] {
+        const char *e = getenv("KG_KEYED");
+        return (e && *e >= '0' && *e <= '2') ? *e - '0' : 2;
+    }();
+    return v;
+}
+
 template <int NR>
 cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedArgs &k, int num_sms, cudaStream_t st) {
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
-    uint64_t want = (dir == 0 && mode == 0) ? a.n_pages : (nb + 255) / 256;
+    const bool chain = (dir == 0 && mode == 0);
+    uint64_t want = chain ? a.n_pages : (nb + 255) / 256;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
     if (want < 1) want = 1;
     const unsigned grid = (unsigned)want;
+    const int v = keyed_variant();
+    if (v > 0 && chain) {
+        if ((a.m & 1) == 0) return launch_pdl_tpb(kg_keyed_chain<NR, true>, grid, kPairThreads, kSmemEnc, st, a, k);
+        return launch_pdl_tpb(kg_keyed_chain<NR, false>, grid, kPairThreads, kSmemEnc, st, a, k);
+    }
+    if (v > 0 && (a.m & 1) == 0) {
+        if (v == 2) {
+            if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 0, true>, grid, kPairThreads, kSmemDec, st, a, k);
+            if (dir == 1) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 1, true>, grid, kPairThreads, kSmemDec, st, a, k);
+            return launch_pdl_tpb(kg_keyed_pair<NR, 0, 1, true>, grid, kPairThreads, kSmemEnc, st, a, k);
+        }
+        if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 0, false>, grid, kPairThreads, kSmemDec, st, a, k);
+        if (dir == 1) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 1, false>, grid, kPairThreads, kSmemDec, st, a, k);
+        return launch_pdl_tpb(kg_keyed_pair<NR, 0, 1, false>, grid, kPairThreads, kSmemEnc, st, a, k);
+    }
     if (dir == 1 && mode == 0) return launch_pdl(kg_keyed<NR, 1, 0>, grid, kSmemDec, st, a, k);
     if (dir == 1) return launch_pdl(kg_keyed<NR, 1, 1>, grid, kSmemDec, st, a, k);
     if (mode == 1) return launch_pdl(kg_keyed<NR, 0, 1>, grid, kSmemEnc, st, a, k);
@@ -727,6 +915,17 @@ cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedA
 }
 
 }  // namespace
+
+bool keyed_uses_const_keys(int dir, int mode, uint32_t m) {
+    return keyed_variant() == 2 && !(dir == 0 && mode == 0) && (m & 1) == 0;
+}
+
+cudaError_t load_const_keys(const DevKeyTable *tab, int dir, cudaStream_t st) {
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_keys, dir == 1 ? (const void *)tab->dec : (const void *)tab->enc,
+                                            sizeof(c_keys), 0, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbolAsync(c_nr, tab->nr, sizeof(c_nr), 0, cudaMemcpyDeviceToDevice, st);
+}
 
 cudaError_t launch_pages_keyed(int dir, int mode, int nr, const LaunchArgs &a, const KeyedArgs &k, int num_sms,
                                cudaStream_t st) {

@@ -79,6 +79,41 @@ struct Slot {
     cudaEvent_t loaded = nullptr, done = nullptr, freed = nullptr;
 };
 
+// The streams that have used a shared device resource (a key-table snapshot,
+// the constant-bank key copy) since it was last (re)filled, one event each:
+// a refill waits for all of them, not just the last recorder.
+struct UseSet {
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> v;
+    cudaError_t record(cudaStream_t st) {
+        for (auto &p : v)
+            if (p.first == st) return cudaEventRecord(p.second, st);
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (r != cudaSuccess) return r;
+        v.push_back({st, e});
+        return cudaEventRecord(e, st);
+    }
+    cudaError_t host_wait() {
+        for (auto &p : v) {
+            cudaError_t r = cudaEventSynchronize(p.second);
+            if (r != cudaSuccess) return r;
+        }
+        return cudaSuccess;
+    }
+    cudaError_t stream_wait(cudaStream_t st) {
+        for (auto &p : v)
+            if (p.first != st) {
+                cudaError_t r = cudaStreamWaitEvent(st, p.second, 0);
+                if (r != cudaSuccess) return r;
+            }
+        return cudaSuccess;
+    }
+    void reset() {
+        for (auto &p : v) cudaEventDestroy(p.second);
+        v.clear();
+    }
+};
+
 constexpr int kMaxSlots = 8;
 constexpr int kKeySnaps = 4;
 constexpr uint32_t kStatusSlots = 1024;
@@ -115,8 +150,14 @@ struct Ctx {
     kg::DevKeyTable *ktab_stage[kKeySnaps] = {};       // pinned staging copies
     kg::DevKeyTable *ktab_dev[kKeySnaps] = {};
     uint64_t ktab_dev_version[kKeySnaps] = {};
-    cudaEvent_t ktab_used[kKeySnaps] = {};
+    UseSet ktab_used[kKeySnaps];
+    cudaEvent_t ktab_ready[kKeySnaps] = {};            // the snapshot's upload (other streams wait on it)
     int ktab_cur = -1;
+    // constant-bank copy of one snapshot's schedules for one direction
+    // (kg::load_const_keys); 0 = empty
+    uint64_t ckeys_version = 0;
+    int ckeys_dir = -1;
+    UseSet ckeys_users;
     uint32_t *status = nullptr;                        // pinned mapped, kStatusSlots words
     uint32_t *status_dev = nullptr;
     bool status_busy[kStatusSlots] = {};
@@ -832,7 +873,7 @@ static int keyed_setup() {
     for (int i = 0; i < kKeySnaps; i++) {
         if (cudaHostAlloc((void **)&g.ktab_stage[i], sizeof(kg::DevKeyTable), 0) != cudaSuccess) goto fail;
         if (cudaMalloc((void **)&g.ktab_dev[i], sizeof(kg::DevKeyTable)) != cudaSuccess) goto fail;
-        if (cudaEventCreateWithFlags(&g.ktab_used[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
+        if (cudaEventCreateWithFlags(&g.ktab_ready[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
         g.ktab_dev_version[i] = 0;
     }
     if (cudaHostAlloc((void **)&g.status, kStatusSlots * sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) goto fail;
@@ -849,15 +890,19 @@ static void keyed_teardown() {
     for (int i = 0; i < kKeySnaps; i++) {
         if (g.ktab_stage[i]) cudaFreeHost(g.ktab_stage[i]);
         if (g.ktab_dev[i]) cudaFree(g.ktab_dev[i]);
-        if (g.ktab_used[i]) cudaEventDestroy(g.ktab_used[i]);
+        g.ktab_used[i].reset();
+        if (g.ktab_ready[i]) cudaEventDestroy(g.ktab_ready[i]);
+        g.ktab_ready[i] = nullptr;
         g.ktab_stage[i] = nullptr;
         g.ktab_dev[i] = nullptr;
-        g.ktab_used[i] = nullptr;
     }
     if (g.status) cudaFreeHost(g.status);
     g.ktab_host = nullptr;
     g.status = g.status_dev = nullptr;
     g.ktab_cur = -1;
+    g.ckeys_users.reset();
+    g.ckeys_version = 0;
+    g.ckeys_dir = -1;
     for (auto &b : g.status_busy) b = false;
 }
 
@@ -865,16 +910,19 @@ static void keyed_teardown() {
 static int keyed_snapshot(cudaStream_t st, const kg::DevKeyTable **out) {
     if (g.ktab_cur >= 0 && g.ktab_dev_version[g.ktab_cur] == g.key_version) {
         *out = g.ktab_dev[g.ktab_cur];
-        KG_CU(cudaEventRecord(g.ktab_used[g.ktab_cur], st));
+        KG_CU(cudaStreamWaitEvent(st, g.ktab_ready[g.ktab_cur], 0));  // uploaded on another stream?
+        KG_CU(g.ktab_used[g.ktab_cur].record(st));
         return KG_OK;
     }
     const int i = (g.ktab_cur + 1) % kKeySnaps;
-    KG_CU(cudaEventSynchronize(g.ktab_used[i]));  // earlier batches done with this snapshot slot
+    KG_CU(g.ktab_used[i].host_wait());  // earlier batches (all streams) done with this snapshot slot
+    g.ktab_used[i].reset();
     memcpy(g.ktab_stage[i], g.ktab_host, sizeof(kg::DevKeyTable));
     KG_CU(cudaMemcpyAsync(g.ktab_dev[i], g.ktab_stage[i], sizeof(kg::DevKeyTable), cudaMemcpyHostToDevice, st));
+    KG_CU(cudaEventRecord(g.ktab_ready[i], st));
     g.ktab_dev_version[i] = g.key_version;
     g.ktab_cur = i;
-    KG_CU(cudaEventRecord(g.ktab_used[i], st));
+    KG_CU(g.ktab_used[i].record(st));
     *out = g.ktab_dev[i];
     return KG_OK;
 }
@@ -934,8 +982,19 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
     k.status = g.status_dev + sslot;
     const int nr = key_bytes / 4 + 6;
     const int sms = g.num_sms;
+    const bool ck = kg::keyed_uses_const_keys(dir, mode, a.m);
+    if (ck && (g.ckeys_version != g.ktab_dev_version[g.ktab_cur] || g.ckeys_dir != dir)) {
+        // refill the constant-bank copy behind every launch still reading it
+        KG_CU(g.ckeys_users.stream_wait(st));
+        g.ckeys_users.reset();
+        g.ckeys_version = 0;
+        KG_CU(kg::load_const_keys(tab, dir, st));
+        g.ckeys_version = g.ktab_dev_version[g.ktab_cur];
+        g.ckeys_dir = dir;
+    }
     cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
+    if (ck) KG_CU(g.ckeys_users.record(st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int64_t t = new_ticket(st);
     if (t >= 0) {

@@ -76,3 +76,47 @@ def test_keyed_errors_and_snapshot():
                                      ids.data_ptr() + 1, 16, None) == kg.EINVAL    # misaligned ids
     assert lib.kg_submit_pages_keyed(1, 0, x.data_ptr(), out.data_ptr(), n, pb, iv.data_ptr(),
                                      ids.data_ptr(), 20, None) == kg.EINVAL        # bad key size
+
+
+def test_keyed_const_keys_cross_stream():
+    """The constant-bank key copy (KG_KEYED=2) is refilled when the snapshot
+    or the direction changes; the refill on one stream must wait for a launch
+    still reading the old copy on another stream."""
+    kg, torch = kg_ready()
+    n, pb = 4096, 4096                         # 16 MiB: long enough to still run when the refill is queued
+    k_a, k_b = synth.make_key(16, seed=31), synth.make_key(16, seed=32)
+    kg.set_key(40, k_a)
+    data = synth.make_pages(n, pb, seed=77)
+    ivs = synth.make_ivs(n, seed=78)
+    x = torch.from_numpy(data).cuda()
+    iv = torch.from_numpy(ivs).cuda()
+    ids = torch.full((n,), 40, dtype=torch.int16, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1, o2, o3 = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    torch.cuda.synchronize()
+    t1 = kg.submit_pages_keyed(1, 0, x, o1, n, pb, iv, ids, 16, s1)      # dec, key A (copy: A/dec)
+    kg.set_key(40, k_b)
+    t2 = kg.submit_pages_keyed(1, 0, x, o2, n, pb, iv, ids, 16, s2)      # dec, key B (refill on s2)
+    t3 = kg.submit_pages_keyed(0, 1, x, o3, n, pb, None, ids, 16, s1)    # ECB enc, key B (refill on s1)
+    for t in (t1, t2, t3):
+        kg.wait(t)
+    torch.cuda.synchronize()
+    assert first_mismatch(o1.cpu().numpy(), oracle_pages(1, 0, k_a, data, n, pb, ivs)) is None
+    assert first_mismatch(o2.cpu().numpy(), oracle_pages(1, 0, k_b, data, n, pb, ivs)) is None
+    assert first_mismatch(o3.cpu().numpy(), oracle_pages(0, 1, k_b, data, n, pb, None)) is None
+
+
+@pytest.mark.parametrize("variant", ["0", "1"])
+def test_keyed_other_variants(variant):
+    """The A/B alternatives behind KG_KEYED (read once per process) stay
+    correct: run a slice of the parity matrix in a child process."""
+    import os
+    import subprocess
+    import sys
+    kg_ready()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KG_KEYED=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_keyed_gpu.py"), "-k", "test_keyed_parity and (37 or 1500)"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
