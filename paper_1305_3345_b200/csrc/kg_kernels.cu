@@ -26,8 +26,9 @@
 //  * Chain kernel (CBC encrypt, serial within a page): one thread per page
 //    chain, pages balanced over a persistent grid of one CTA per SM; two
 //    blocks per 256-bit L1::no_allocate load/store (measured, profiles/r1_ldst).
-//  * Mixed-key kernel: same bodies, round keys per lane from a device
-//    snapshot of the key table.
+//  * Mixed-key kernels: same bodies; round keys of the lane's page from a
+//    constant-bank copy of the key-table snapshot (block pairs: LDC, off the
+//    saturated L1 data pipe) or in registers per page (CBC-encrypt chains).
 //  * Launches use programmatic dependent launch: the table fill runs before
 //    griddepcontrol.wait.
 //  * In-place safety (out == in): CTAs own whole pages; inside a CTA every
