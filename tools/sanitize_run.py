@@ -32,6 +32,20 @@ for n, pb in [(3, 4096), (5, 48), (40, 512)]:
                     kg.wait(kg.submit_pages(d, mode, hdata, hout, n, pb, hivs if mode == 0 else None, kb))
                     assert torch.equal(hout.cuda(), out)
                 kg.set_host_path(kg.HOST_AUTO)
+# mixed-key batches: block pairs with constant-bank keys, register-key chains, odd-m kernel
+for i, kid in enumerate((3, 7, 9)):
+    kg.set_key(kid, synth.make_key(16, seed=50 + i))
+for n, pb in [(3, 4096), (5, 48), (40, 512)]:
+    data = torch.from_numpy(synth.make_pages(n, pb)).cuda()
+    ivs = torch.from_numpy(synth.make_ivs(n)).cuda()
+    ids = torch.tensor([(3, 7, 9)[p % 3] for p in range(n)], dtype=torch.int16, device="cuda")
+    for d in (0, 1):
+        for mode in (0, 1):
+            out = torch.empty_like(data)
+            kg.wait(kg.submit_pages_keyed(d, mode, data, out, n, pb, ivs if mode == 0 else None, ids, 16))
+            x = data.clone()
+            kg.wait(kg.submit_pages_keyed(d, mode, x, x, n, pb, ivs if mode == 0 else None, ids, 16))
+            assert torch.equal(x, out)
 kg.nsk_start(2, kg.NSK_DIRECT, 2000)
 n, pb = 4, 4096
 data = torch.from_numpy(synth.make_pages(n, pb)).cuda()
