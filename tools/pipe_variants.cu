@@ -8,6 +8,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+#include <thread>
 #include <vector>
 
 __global__ void noop_kernel(uint4 *p, size_t n) {
@@ -21,6 +23,17 @@ __global__ void touch(uint4 *p, size_t n) {
         v.x ^= 1;
         p[i] = v;
     }
+}
+
+// occupies every SM for ~ns (optionally with a large dynamic smem allocation)
+__global__ void spin(unsigned long long ns) {
+    extern __shared__ char smem_dummy[];
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+    if (threadIdx.x == 5000) smem_dummy[0] = 1;
 }
 
 // persistent: processes chunk c once flag_in[c] == 1 (set by the H2D stream
@@ -75,8 +88,10 @@ int main() {
     cudaEventCreate(&th);
     cudaEventCreate(&td);
     const char *names[] = {"copies_no_deps", "events_no_kernel", "events_noop_kernel", "events_touch_kernel",
-                           "memops_persistent_kernel"};
-    for (int v = 0; v < 5; v++) {
+                           "memops_persistent_kernel", "events_spin30us_nosmem", "events_spin30us_smem196K",
+                           "events_spin30us_smem196K_1cta", "events_spin10us_smem196K"};
+    cudaFuncSetAttribute(spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 196608);
+    for (int v = 0; v < 9; v++) {
         float best = 1e9f, besth = 1e9f;
         for (int rep = 0; rep < 5; rep++) {
             cudaMemset(flags, 0, 3 * 64 * sizeof(uint32_t));
@@ -97,7 +112,11 @@ int main() {
                     if (v >= 2) {
                         cudaStreamWaitEvent(sk, loaded[i], 0);
                         if (v == 2) noop_kernel<<<1, 32, 0, sk>>>((uint4 *)st, chunk / 16);
-                        else touch<<<148, 1024, 0, sk>>>((uint4 *)st, chunk / 16);
+                        else if (v == 3) touch<<<148, 1024, 0, sk>>>((uint4 *)st, chunk / 16);
+                        else if (v == 5) spin<<<148, 512, 0, sk>>>(30000);
+                        else if (v == 6) spin<<<148, 512, 196608, sk>>>(30000);
+                        else if (v == 7) spin<<<1, 512, 196608, sk>>>(30000);
+                        else spin<<<148, 512, 196608, sk>>>(10000);
                         cudaEventRecord(done[i], sk);
                         cudaStreamWaitEvent(sd, done[i], 0);
                     } else {
@@ -118,6 +137,49 @@ int main() {
                names[v], best, total / (best * 1e-3) / 1e9, total / (besth * 1e-3) / 1e9);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e));
+    }
+    // host-issued D2H: a second host thread waits for each chunk's kernel and only
+    // then enqueues its D2H, so the D2H channel never holds a semaphore wait
+    const int spins[] = {30000, 0, 5000, 10000, 20000, 30000, 50000, -1, -2};
+    for (int kx = 0; kx < 9; kx++) {
+        const int kk = spins[kx] >= 0 ? 0 : (spins[kx] == -1 ? 1 : 2);
+        float best = 1e9f, besth = 1e9f;
+        for (int rep = 0; rep < 5; rep++) {
+            cudaDeviceSynchronize();
+            cudaEventRecord(t0, sh);
+            cudaStreamWaitEvent(sk, t0, 0);
+            std::atomic<int> recorded{0};  // events of this rep recorded so far (no stale-event race)
+            std::thread issuer([&] {
+                for (int i = 0; i < nch; i++) {
+                    while (recorded.load(std::memory_order_acquire) <= i) std::this_thread::yield();
+                    cudaEventSynchronize(kk == 2 ? loaded[i] : done[i]);
+                    cudaMemcpyAsync(hout + i * chunk, dstage + i * chunk, chunk, cudaMemcpyDeviceToHost, sd);
+                }
+                cudaEventRecord(td, sd);
+            });
+            for (int i = 0; i < nch; i++) {
+                uint8_t *st = dstage + i * chunk;
+                cudaMemcpyAsync(st, hin + i * chunk, chunk, cudaMemcpyHostToDevice, sh);
+                cudaEventRecord(loaded[i], sh);
+                if (kk < 2) {
+                    cudaStreamWaitEvent(sk, loaded[i], 0);
+                    if (kk == 0) spin<<<148, 512, 196608, sk>>>(spins[kx]);
+                    else touch<<<148, 1024, 0, sk>>>((uint4 *)st, chunk / 16);
+                    cudaEventRecord(done[i], sk);
+                }
+                recorded.store(i + 1, std::memory_order_release);
+            }
+            cudaEventRecord(th, sh);
+            issuer.join();
+            cudaDeviceSynchronize();
+            float ms, msh;
+            cudaEventElapsedTime(&ms, t0, td);
+            cudaEventElapsedTime(&msh, t0, th);
+            if (ms < best) best = ms, besth = msh;
+        }
+        const char *nm[] = {"host_issued_d2h_spin", "host_issued_d2h_touch", "host_issued_d2h_no_kernel"};
+        printf("{\"variant\": \"%s\", \"spin_ns\": %d, \"chunk_mib\": 16, \"ms\": %.3f, \"gbs\": %.2f, \"h2d_stream_gbs\": %.2f}\n",
+               nm[kk], spins[kx], best, total / (best * 1e-3) / 1e9, total / (besth * 1e-3) / 1e9);
     }
     return 0;
 }
