@@ -41,8 +41,8 @@
  * GPU (or managed memory) or page-locked ("pinned") host memory registered
  * with CUDA.  Pageable host memory -> KG_EINVAL.  Mixed kinds are allowed.
  * Device batches run on `stream`; batches touching host memory are staged
- * through the library's device staging ring (3 slots by default, after
- * PAPER.md:437-440) on internal copy/compute streams overlapped with each
+ * through the library's device staging ring (4 slots by default, after
+ * PAPER.md:437-440's three buffers plus one) on internal copy/compute streams overlapped with each
  * other, joined back onto `stream`.
  */
 #ifndef KG_H
@@ -154,9 +154,11 @@ KG_API int kg_shutdown(void);
 KG_API const char *kg_strerror(int status);
 
 /* Staging pipeline for batches touching host memory: chunk size in bytes
- * (rounded down to whole pages, at least one page) and number of device
- * staging slots (2..8).  Takes effect for later submits.  Defaults: 16 MiB,
- * 3 slots ("three buffers").  Environment overrides at
+ * (rounded down to whole pages, at least one page; 0 = auto: 8 MiB, or
+ * 16 MiB for CBC encryption, whose per-page chains need the longer copy to
+ * hide behind) and number of device staging slots (2..8).  Takes effect for
+ * later submits.  Defaults: auto, 4 slots (PAPER.md:437-440's "three buffers" plus one: the D2H of a chunk
+ * is held back until the next chunk's H2D has landed, profiles/r1_pinned).  Environment overrides at
  * kg_init: KG_CHUNK_BYTES, KG_STAGING_SLOTS.  KG_EINVAL on bad values. */
 KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);
 

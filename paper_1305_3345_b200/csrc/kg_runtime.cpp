@@ -12,8 +12,9 @@
 //    concurrently with another service running on the GPU" and "on the GPU,
 //    we use three buffers ... one is used by the active service, a second
 //    may receive input ... a third may be copying the output" -> host-memory
-//    batches stream through a ring of device staging slots (default 3) on an
-//    H2D stream, a compute stream and a D2H stream ordered by events.
+//    batches stream through a ring of device staging slots (default 4: the
+//    paper's three plus one for the lagged D2H) on an H2D stream, a compute
+//    stream and a D2H stream ordered by events.
 //  * There is no user-space helper process and no kernel module: one address
 //    space, so the copy engines DMA straight from/to the caller's pinned
 //    pages (the paper's own §4 "save an extra copy" idea).
@@ -130,8 +131,12 @@ struct Ctx {
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_begin = nullptr;
     Slot slots[kMaxSlots];
-    uint64_t chunk_bytes = 16ull << 20;
-    int n_slots = 3;
+    // 0 = auto: 8 MiB for block-parallel kernels, 16 MiB for CBC-encrypt
+    // chains (whose per-chunk kernel is latency-bound at ~90 us below ~74 MiB,
+    // so it needs the longer copy to hide behind); measured with the lagged
+    // D2H, profiles/r1_pinned/README.md
+    uint64_t chunk_bytes = 0;
+    int n_slots = 4;
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
     // batch IVs of host batches (<= kIvStageMax), double-buffered: a buffer is
@@ -352,7 +357,9 @@ int ensure_iv_stage(int b, uint64_t bytes) {
 int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint8_t *in, Kind kin,
                   uint8_t *out, Kind kout, uint64_t n_pages, uint32_t page_bytes, const uint8_t *ivs,
                   Kind kiv, cudaStream_t st) {
-    uint64_t chunk_pages = g.chunk_bytes / page_bytes;
+    const uint64_t cb = g.chunk_bytes ? g.chunk_bytes
+                        : (dir == KG_ENCRYPT && mode == KG_MODE_CBC) ? (16ull << 20) : (8ull << 20);
+    uint64_t chunk_pages = cb / page_bytes;
     if (chunk_pages < 1) chunk_pages = 1;
     if (chunk_pages > n_pages) chunk_pages = n_pages;
     const bool need_iv = (mode == KG_MODE_CBC);
@@ -384,7 +391,11 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         std::vector<uint64_t> ramp;
         if (n_pages >= 4 * chunk_pages && chunk_pages >= 8)
             for (uint64_t d = 8; d >= 2; d /= 2) ramp.push_back(chunk_pages / d);
-        for (uint64_t r : ramp) sched.push_back(r), left -= 2 * r;
+        static const bool ramp_down = [] {
+            const char *e = getenv("KG_RAMP_DOWN");
+            return !(e && *e == '0');
+        }();
+        for (uint64_t r : ramp) sched.push_back(r), left -= ramp_down ? 2 * r : r;
         std::vector<uint64_t> mid;
         while (left > 0) {
             const uint64_t np = left < chunk_pages ? left : chunk_pages;
@@ -392,10 +403,37 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
             left -= np;
         }
         sched.insert(sched.end(), mid.begin(), mid.end());
-        for (size_t r = ramp.size(); r-- > 0;) sched.push_back(ramp[r]);
+        if (ramp_down)
+            for (size_t r = ramp.size(); r-- > 0;) sched.push_back(ramp[r]);
     }
-    uint64_t p0 = 0;
-    for (uint64_t i = 0; i < sched.size(); p0 += sched[i], ++i) {
+    // D2H of chunk i is held back until the H2D of chunk i+1 has landed, so
+    // that it starts together with the H2D of chunk i+2.  The copy engines
+    // otherwise fall into lock-step with the kernel in between: every chunk's
+    // compute time was added to the link time (profiles/r1_pinned/README.md,
+    // "lagged_d2h": the H2D stream back at the contended link rate).
+    // KG_D2H_LAG: 0 = off, 1 (default) = every chunk, 2 = only when the next
+    // chunk has the same size (measured: 1 and 2 within noise, 0 -4%)
+    static const int lag_mode = [] {
+        const char *e = getenv("KG_D2H_LAG");
+        return (e && *e >= '0' && *e <= '2') ? *e - '0' : 1;
+    }();
+    const bool lag = lag_mode != 0;
+    auto lag_on = [&](uint64_t j) {
+        return lag && j + 1 < sched.size() && (lag_mode == 1 || sched[j + 1] == sched[j]);
+    };
+    auto d2h = [&](uint64_t j, uint64_t pj) -> int {  // D2H stage of chunk j (first page pj)
+        Slot &s = g.slots[j % (uint64_t)g.n_slots];
+        KG_CU(cudaStreamWaitEvent(g.s_d2h, s.done, 0));
+        if (lag_on(j)) KG_CU(cudaStreamWaitEvent(g.s_d2h, g.slots[(j + 1) % (uint64_t)g.n_slots].loaded, 0));
+        if (kout == K_HOST)
+            KG_CU(cudaMemcpyAsync(out + pj * page_bytes, s.data, sched[j] * page_bytes, cudaMemcpyDeviceToHost,
+                                  g.s_d2h));
+        KG_CU(cudaEventRecord(s.freed, g.s_d2h));
+        trace(j, 'd', g.s_d2h);
+        return KG_OK;
+    };
+    uint64_t p0 = 0, p_prev = 0;
+    for (uint64_t i = 0; i < sched.size(); p_prev = p0, p0 += sched[i], ++i) {
         const uint64_t np = sched[i];
         const uint64_t off = p0 * page_bytes, nbytes = np * page_bytes;
         Slot &s = g.slots[i % (uint64_t)g.n_slots];
@@ -406,6 +444,8 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
             KG_CU(cudaMemcpyAsync(s.ivs, ivs + 16 * p0, 16 * np, cudaMemcpyHostToDevice, g.s_h2d));
         KG_CU(cudaEventRecord(s.loaded, g.s_h2d));
         trace(i, 'h', g.s_h2d);
+        // the previous chunk's D2H (needs this chunk's loaded event when lagged)
+        if (lag && i > 0 && (rc = d2h(i - 1, p_prev)) != KG_OK) return rc;
         // compute stage
         KG_CU(cudaStreamWaitEvent(g.s_comp, s.loaded, 0));
         kg::LaunchArgs a;
@@ -422,12 +462,9 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         if (rc != KG_OK) return rc;
         KG_CU(cudaEventRecord(s.done, g.s_comp));
         trace(i, 'k', g.s_comp);
-        // D2H stage
-        KG_CU(cudaStreamWaitEvent(g.s_d2h, s.done, 0));
-        if (kout == K_HOST) KG_CU(cudaMemcpyAsync(out + off, s.data, nbytes, cudaMemcpyDeviceToHost, g.s_d2h));
-        KG_CU(cudaEventRecord(s.freed, g.s_d2h));
-        trace(i, 'd', g.s_d2h);
+        if (!lag && (rc = d2h(i, p0)) != KG_OK) return rc;
     }
+    if (lag && (rc = d2h(sched.size() - 1, p_prev)) != KG_OK) return rc;
     if (iv_upfront) KG_CU(cudaEventRecord(g.iv_free[ivb], g.s_comp));
     // join: the caller's stream continues after the last D2H
     KG_CU(cudaEventRecord(g.ev_begin, g.s_d2h));
@@ -636,7 +673,7 @@ int kg_init(int device) {
 int kg_set_pipeline(uint64_t chunk_bytes, int slots) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g.up) return KG_ENOTINIT;
-    if (chunk_bytes < 16 || slots < 2 || slots > kMaxSlots) return KG_EINVAL;
+    if ((chunk_bytes != 0 && chunk_bytes < 16) || slots < 2 || slots > kMaxSlots) return KG_EINVAL;
     if (slots != g.n_slots) {
         cudaStreamSynchronize(g.s_h2d);
         cudaStreamSynchronize(g.s_comp);

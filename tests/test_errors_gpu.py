@@ -93,7 +93,7 @@ def test_init_other_device_rejected(env):
     lib = kg.raw_lib()
     assert lib.kg_init(0) == kg.OK          # idempotent
     assert lib.kg_init(1 if torch.cuda.device_count() > 1 else 999) == kg.EINVAL
-    assert lib.kg_set_pipeline(0, 3) == kg.EINVAL
+    assert lib.kg_set_pipeline(8, 3) == kg.EINVAL          # 0 = auto is valid; 1..15 are not
     assert lib.kg_set_pipeline(1 << 20, 1) == kg.EINVAL
     assert lib.kg_set_pipeline(1 << 20, 9) == kg.EINVAL
 

@@ -96,12 +96,12 @@ def test_small_staging_chunks_many_slots():
     ivs = synth.make_ivs(n, seed=7)
     exp = oracle_pages(1, 0, key, data, n, pb, ivs)
     kg.set_host_path(kg.HOST_STAGED)
-    for chunk, slots in [(4096, 2), (3 * 4096, 3), (64 * 1024, 8), (10 * 4096 + 16, 3)]:
+    for chunk, slots in [(4096, 2), (3 * 4096, 3), (64 * 1024, 8), (10 * 4096 + 16, 3), (0, 4), (0, 2)]:
         kg.set_pipeline(chunk, slots)
         try:
             got = gpu_pages(1, 0, key, data, n, pb, ivs, where="pinned")
         finally:
-            kg.set_pipeline(16 << 20, 3)
+            kg.set_pipeline(0, 4)
             kg.set_host_path(kg.HOST_AUTO, 32 << 20)
         assert first_mismatch(got, exp) is None, (chunk, slots)
 
@@ -185,7 +185,7 @@ def test_staged_batches_back_to_back():
             exp = oracle_pages(d, 0, key, data, n, pb, ivs)
             assert first_mismatch(hout.numpy(), exp) is None
     finally:
-        kg.set_pipeline(16 << 20, 3)
+        kg.set_pipeline(0, 4)
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
 
 
@@ -205,3 +205,21 @@ def test_tail_pool_large_batches(pb, inplace):
     exp_e = oracle_pages(1, 1, key, data, n, pb, None)
     got_e = gpu_pages(1, 1, key, data, n, pb, None, where="device", inplace=inplace)
     assert first_mismatch(got_e, exp_e) is None
+
+
+@pytest.mark.parametrize("lag", ["0", "2"])
+def test_staged_d2h_lag_modes(lag):
+    """The staged pipeline's D2H lag modes other than the default (KG_D2H_LAG,
+    read once per process): the staged parity cases in a child process."""
+    import os
+    import subprocess
+    import sys
+    from gpu_util import kg_ready
+    kg_ready()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KG_D2H_LAG=lag, KG_RAMP_DOWN="0" if lag == "2" else "1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_parity_gpu.py"),
+                        "-k", "(staged_batches or small_staging or cbc_pinned or mixed_residency) and not lag_modes"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -89,9 +89,10 @@ int main() {
     cudaEventCreate(&td);
     const char *names[] = {"copies_no_deps", "events_no_kernel", "events_noop_kernel", "events_touch_kernel",
                            "memops_persistent_kernel", "events_spin30us_nosmem", "events_spin30us_smem196K",
-                           "events_spin30us_smem196K_1cta", "events_spin10us_smem196K"};
+                           "events_spin30us_smem196K_1cta", "events_spin10us_smem196K",
+                           "lagged_d2h_spin30us", "lagged_d2h_touch", "lagged2_d2h_spin30us"};
     cudaFuncSetAttribute(spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 196608);
-    for (int v = 0; v < 9; v++) {
+    for (int v = 0; v < 12; v++) {
         float best = 1e9f, besth = 1e9f;
         for (int rep = 0; rep < 5; rep++) {
             cudaMemset(flags, 0, 3 * 64 * sizeof(uint32_t));
@@ -101,7 +102,28 @@ int main() {
             cudaStreamWaitEvent(sd, t0, 0);
             if (v == 4)
                 persistent<<<148, 1024, 0, sk>>>(dstage, chunk, nch, flags, flags + 64, flags + 128);
-            for (int i = 0; i < nch; i++) {
+            if (v >= 9) {
+                // D2H(i) additionally waits for H2D(i+lag): the D2H of a chunk starts together
+                // with an H2D, never in the middle of one
+                const int lag = v == 11 ? 2 : 1;
+                for (int i = 0; i < nch + lag; i++) {
+                    if (i < nch) {
+                        cudaMemcpyAsync(dstage + i * chunk, hin + i * chunk, chunk, cudaMemcpyHostToDevice, sh);
+                        cudaEventRecord(loaded[i], sh);
+                        cudaStreamWaitEvent(sk, loaded[i], 0);
+                        if (v == 10) touch<<<148, 1024, 0, sk>>>((uint4 *)(dstage + i * chunk), chunk / 16);
+                        else spin<<<148, 512, 196608, sk>>>(30000);
+                        cudaEventRecord(done[i], sk);
+                    }
+                    const int j = i - lag;
+                    if (j >= 0) {
+                        cudaStreamWaitEvent(sd, done[j], 0);
+                        if (i < nch) cudaStreamWaitEvent(sd, loaded[i], 0);
+                        cudaMemcpyAsync(hout + j * chunk, dstage + j * chunk, chunk, cudaMemcpyDeviceToHost, sd);
+                    }
+                }
+            }
+            for (int i = 0; i < nch && v < 9; i++) {
                 uint8_t *st = dstage + i * chunk;
                 cudaMemcpyAsync(st, hin + i * chunk, chunk, cudaMemcpyHostToDevice, sh);
                 if (v == 4) {
