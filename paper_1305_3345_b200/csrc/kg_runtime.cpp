@@ -391,11 +391,15 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         std::vector<uint64_t> ramp;
         if (n_pages >= 4 * chunk_pages && chunk_pages >= 8)
             for (uint64_t d = 8; d >= 2; d /= 2) ramp.push_back(chunk_pages / d);
-        static const bool ramp_down = [] {
+        // KG_RAMP_DOWN = number of ramp levels at the end (0..3, default 3:
+        // C/2, C/4, C/8); the ramp-up is always C/8, C/4, C/2
+        static const size_t down = [] {
             const char *e = getenv("KG_RAMP_DOWN");
-            return !(e && *e == '0');
+            return (e && *e >= '0' && *e <= '3') ? (size_t)(*e - '0') : (size_t)3;
         }();
-        for (uint64_t r : ramp) sched.push_back(r), left -= ramp_down ? 2 * r : r;
+        const size_t nd = down < ramp.size() ? down : ramp.size();
+        for (uint64_t r : ramp) sched.push_back(r), left -= r;
+        for (size_t r = ramp.size() - nd; r < ramp.size(); ++r) left -= ramp[r];
         std::vector<uint64_t> mid;
         while (left > 0) {
             const uint64_t np = left < chunk_pages ? left : chunk_pages;
@@ -403,8 +407,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
             left -= np;
         }
         sched.insert(sched.end(), mid.begin(), mid.end());
-        if (ramp_down)
-            for (size_t r = ramp.size(); r-- > 0;) sched.push_back(ramp[r]);
+        for (size_t r = ramp.size(); r-- > ramp.size() - nd;) sched.push_back(ramp[r]);
     }
     // D2H of chunk i is held back until the H2D of chunk i+1 has landed, so
     // that it starts together with the H2D of chunk i+2.  The copy engines
