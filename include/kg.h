@@ -125,8 +125,9 @@ KG_API int64_t kg_submit_pages(int dir, int mode, const void *in, void *out,
  * blocks of different tasks"): as kg_submit_pages, but page
  * p uses key key_ids[p] (uint16 per page, 2-byte aligned, device or pinned
  * host memory).  Every referenced key must be set and key_bytes long; the
- * key table is snapshotted at submit.  Host buffers are read/written in place
- * (zero-copy).  A page naming an unset key or a key of another size makes
+ * key table is snapshotted at submit.  Host buffers take the same host path
+ * as in kg_submit_pages (zero-copy, or the staging pipeline with each
+ * chunk's launch reading its slice of key_ids).  A page naming an unset key or a key of another size makes
  * kg_wait return KG_ENOKEY (that page's output is unspecified).
  * Errors: as kg_submit_pages, plus KG_EINVAL for bad key_bytes or key_ids,
  * KG_ENOTSUP while the NSK runs. */

@@ -354,9 +354,11 @@ int ensure_iv_stage(int b, uint64_t bytes) {
     return KG_OK;
 }
 
+// keyed != nullptr: a mixed-key batch (key_ids device-usable, indexed from
+// the batch's first page); each chunk's launch gets its slice of the ids.
 int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint8_t *in, Kind kin,
                   uint8_t *out, Kind kout, uint64_t n_pages, uint32_t page_bytes, const uint8_t *ivs,
-                  Kind kiv, cudaStream_t st) {
+                  Kind kiv, cudaStream_t st, const kg::KeyedArgs *keyed = nullptr) {
     const uint64_t cb = g.chunk_bytes ? g.chunk_bytes
                         : (dir == KG_ENCRYPT && mode == KG_MODE_CBC) ? (16ull << 20) : (8ull << 20);
     uint64_t chunk_pages = cb / page_bytes;
@@ -461,8 +463,16 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         a.m = page_bytes / 16;
         a.in_place = (const void *)a.in == (const void *)a.out;
         a.rk = rk;
-        rc = launch(dir, mode, nr, a, g.s_comp);
-        if (rc != KG_OK) return rc;
+        if (keyed) {
+            kg::KeyedArgs k = *keyed;
+            k.key_ids += p0;
+            cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, g.num_sms, g.s_comp);
+            if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+        } else {
+            rc = launch(dir, mode, nr, a, g.s_comp);
+            if (rc != KG_OK) return rc;
+        }
         KG_CU(cudaEventRecord(s.done, g.s_comp));
         trace(i, 'k', g.s_comp);
         if (!lag && (rc = d2h(i, p0)) != KG_OK) return rc;
@@ -988,8 +998,17 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
     const Kind kin = classify(in, &zin), kout = classify(out, &zout), kid = classify(key_ids, &zid),
                kiv = need_iv ? classify(ivs, &ziv) : K_DEVICE;
     if (kin == K_BAD || kout == K_BAD || kiv == K_BAD || kid == K_BAD) return KG_EINVAL;
-    // keyed batches run in one launch: host buffers are accessed in place
-    if (!zin || !zout || !zid || (need_iv && !ziv)) return KG_EINVAL;
+    // The ids are read by the kernels wherever they live (device memory or the
+    // device alias of pinned memory).  Batches touching host memory follow the
+    // kg_submit_pages host-path rule: zero-copy (one launch on the caller's
+    // pinned pages) or the staging pipeline.
+    if (!zid) return KG_EINVAL;
+    const bool all_device = (kin == K_DEVICE && kout == K_DEVICE && kiv == K_DEVICE);
+    const bool chain = (dir == KG_ENCRYPT && mode == KG_MODE_CBC);
+    const bool zero_copy = !all_device && zin && zout && (!need_iv || ziv) &&
+                           (g.host_path == KG_HOST_ZEROCOPY ||
+                            (g.host_path == KG_HOST_AUTO && !chain && total <= g.zc_max_bytes));
+    const bool staged = !all_device && !zero_copy;
     if (g.tickets.size() >= (size_t)KG_MAX_INFLIGHT) return KG_EAGAIN;
     int rc = keyed_setup();
     if (rc != KG_OK) return rc;
@@ -1032,10 +1051,20 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
         g.ckeys_version = g.ktab_dev_version[g.ktab_cur];
         g.ckeys_dir = dir;
     }
-    cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, st);
-    if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
+    if (staged) {
+        // chunk launches run on the internal compute stream, forked from and
+        // joined back onto `st`: the snapshot / constant-key uses are
+        // recorded on `st` after the join
+        rc = submit_staged(dir, mode, nr, a.rk, (const uint8_t *)in, kin, (uint8_t *)out, kout, n_pages, page_bytes,
+                           (const uint8_t *)ivs, kiv, st, &k);
+        if (rc != KG_OK) return rc;
+        KG_CU(g.ktab_used[g.ktab_cur].record(st));
+    } else {
+        cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
     if (ck) KG_CU(g.ckeys_users.record(st));
-    g_launches.fetch_add(1, std::memory_order_relaxed);
     const int64_t t = new_ticket(st);
     if (t >= 0) {
         g.tickets[t].status_slot = (int)sslot;

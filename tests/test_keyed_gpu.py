@@ -120,3 +120,41 @@ def test_keyed_other_variants(variant):
                         os.path.join(root, "tests", "test_keyed_gpu.py"), "-k", "test_keyed_parity and (37 or 1500)"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("direction,mode", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("path", ["staged", "auto"])
+def test_keyed_host_batches(direction, mode, path):
+    """Mixed-key batches with pinned host pages (rows f1 x f4): through the
+    staging pipeline (chunk launches each read their slice of the ids) or,
+    under AUTO, zero-copy below the threshold and staged above it."""
+    kg, torch = kg_ready()
+    key_set = [3, 77, 254]
+    keys = {}
+    for i, kid in enumerate(key_set):
+        keys[kid] = synth.make_key(16, seed=900 + i)
+        kg.set_key(kid, keys[kid])
+    n, pb = (9000, 4096) if path == "auto" else (1500, 4096)   # auto: 35 MiB > the 32 MiB zero-copy cap
+    rng = np.random.default_rng(n + direction * 2 + mode)
+    ids = np.array(key_set, dtype=np.uint16)[rng.integers(0, len(key_set), n)]
+    data = synth.make_pages(n, pb, seed=n + 11)
+    ivs = synth.make_ivs(n, seed=n + 12) if mode == 0 else None
+    exp = expected(direction, mode, keys, ids, data, n, pb, ivs)
+    hin = torch.from_numpy(data).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    hid = torch.from_numpy(ids.astype(np.int16)).pin_memory()
+    hiv = None if ivs is None else torch.from_numpy(ivs).pin_memory()
+    if path == "staged":
+        kg.set_host_path(kg.HOST_STAGED)
+        kg.set_pipeline(64 * 4096, 3)           # many chunks, slots wrap
+    try:
+        kg.wait(kg.submit_pages_keyed(direction, mode, hin, hout, n, pb, hiv, hid, 16))
+        assert first_mismatch(hout.numpy(), exp) is None
+        # in place, ids in device memory
+        y = hin.clone().pin_memory()
+        did = hid.cuda()
+        kg.wait(kg.submit_pages_keyed(direction, mode, y, y, n, pb, hiv, did, 16))
+        assert first_mismatch(y.numpy(), exp) is None
+    finally:
+        kg.set_pipeline(0, 4)
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)
