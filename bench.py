@@ -331,9 +331,11 @@ def run_ours(args):
     elapsed = starts[0].elapsed_time(ends[-1]) / 1e3                   # s, device-timed
     if args.step_events:
         per_launch = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
-        avg_launch = sum(per_launch) / len(per_launch)
+        avg_launch = sum(per_launch) / max(launches, len(per_launch))
     else:
-        avg_launch = elapsed / args.steps  # one launch per step, back to back on one stream
+        # launches back to back on one stream; a step is one launch, or several
+        # page windows when the input exceeds one texture (C5)
+        avg_launch = elapsed / max(launches, args.steps)
     if dist:
         t = torch.tensor([elapsed, avg_launch], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -396,7 +398,9 @@ def run_ours(args):
 
     peaks = load_peaks()
     sm_max = float(clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
-    achieved = bytes_step / avg_launch / 1e9
+    launches_per_step = max(1, launches // args.steps)
+    bytes_launch = bytes_step / launches_per_step
+    achieved = bytes_launch / avg_launch / 1e9
     peak = compute_peak_gbs(key_bytes, sm_max)
     roof = {
         "bound": "alu", "pipe": "lds (shared-memory T-table lookups: 16*Nr lane-lookups per 16-byte block)",
@@ -409,7 +413,8 @@ def run_ours(args):
         "hbm_frac": achieved / (peaks["hbm_gbs"] / (2 + 16.0 / PB)),
         "kernel": (("kg_keyed_chain" if (direction == 0 and mode == kg.MODE_CBC) else "kg_keyed_pair") if keyed
                    else "kg_blockpar" if (direction == 1 or mode == kg.MODE_ECB) else "kg_cbc_enc") + f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>",
-        "algorithmic_bytes_per_launch": bytes_step,
+        "algorithmic_bytes_per_launch": bytes_launch,
+        "launches_per_step": launches_per_step,
     }
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,

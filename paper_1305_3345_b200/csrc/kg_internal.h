@@ -30,6 +30,12 @@ struct LaunchArgs {
     uint32_t m;           // blocks per page = page_bytes / 16
     uint32_t in_place;    // out == in
     RoundKeys rk;
+    // Optional: a 1D linear texture (uint4 elements) over the input, so the
+    // block-pair kernel's page loads use the TEX data pipe instead of the LSU
+    // one the table lookups saturate (profiles/r1_tex).  in[i] is texel
+    // tex_off + i.  0 = plain global loads.
+    unsigned long long tex_in = 0;
+    int64_t tex_off = 0;
 };
 
 // Base (unreplicated) lookup tables, built on the host by the GPU-path code

@@ -243,7 +243,22 @@ struct Job {
     uint64_t n_pages;
     uint32_t m;
     uint32_t in_place;
+    unsigned long long tex = 0;  // see LaunchArgs::tex_in
+    int64_t tex_off = 0;
 };
+
+// The two input blocks of pair q (blocks 2q, 2q+1): one LDG.256, or (TEX)
+// two texel fetches through the texture pipe.
+template <bool TEX>
+__device__ __forceinline__ void ld_pair(const Job &a, uint64_t q, uint4 &x0, uint4 &x1) {
+    if (TEX) {
+        const int i = (int)(a.tex_off + 2 * (int64_t)q);
+        x0 = tex1Dfetch<uint4>((cudaTextureObject_t)a.tex, i);
+        x1 = tex1Dfetch<uint4>((cudaTextureObject_t)a.tex, i + 1);
+    } else {
+        ld256<false>(a.in + 2 * q, x0, x1);
+    }
+}
 
 // ---- block-parallel body: CBC decrypt, ECB decrypt, ECB encrypt ---------------
 // CTA `cta` of `ncta` processes its balanced share of the batch; each warp
@@ -323,7 +338,7 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
 
 // Stream the pairs [w0, w1) of one warp.  (n0, n1) holds the warp's first
 // unit (already loaded); carry = C of the block before w0 (if not a page start).
-template <bool DEC, bool CBC, class Cipher>
+template <bool DEC, bool CBC, bool TEX, class Cipher>
 __device__ __forceinline__ void pair_stream(const Job &a, const Cipher &cph, uint64_t w0, uint64_t w1, uint64_t mp,
                                             uint4 carry, uint64_t page, uint32_t jp, uint4 n0, uint4 n1) {
     const uint32_t lane = threadIdx.x & 31;
@@ -331,7 +346,7 @@ __device__ __forceinline__ void pair_stream(const Job &a, const Cipher &cph, uin
         const uint64_t q = u + lane;
         const bool act = q < w1;
         const uint4 x0 = n0, x1 = n1;
-        if (q + 32 < w1) ld256<false>(a.in + 2 * (q + 32), n0, n1);
+        if (q + 32 < w1) ld_pair<TEX>(a, q + 32, n0, n1);
         uint4 prev = make_uint4(0, 0, 0, 0);
         if (CBC && DEC) {
             const uint4 r = shfl4(x1, (lane + 31) & 31);
@@ -368,7 +383,7 @@ __device__ __forceinline__ void pair_stream(const Job &a, const Cipher &cph, uin
 // (the unit's CBC predecessor is re-read from `in`, which nobody writes),
 // whole pages in place (the IV starts each page, so no predecessor crosses
 // warps).
-template <bool DEC, bool CBC, class Cipher>
+template <bool DEC, bool CBC, bool TEX = false, class Cipher>
 __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
     __shared__ unsigned long long pool_next;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -397,9 +412,9 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
         if (w0 < w1 && (w0 % mp) != 0) carry = a.in[2 * w0 - 1];
     }
     uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-    if (w0 + lane < w1) ld256<false>(a.in + 2 * (w0 + lane), n0, n1);
+    if (w0 + lane < w1) ld_pair<TEX>(a, w0 + lane, n0, n1);
     __syncthreads();
-    pair_stream<DEC, CBC>(a, cph, w0, w1, mp, carry, page, jp, n0, n1);
+    pair_stream<DEC, CBC, TEX>(a, cph, w0, w1, mp, carry, page, jp, n0, n1);
     if (!pool) return;
     const uint64_t unit = a.in_place ? mp : 32;  // pairs per claim
     for (;;) {
@@ -411,11 +426,11 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
         // when mp is not a multiple of 32)
         const uint64_t pg = (q0 + lane) / mp;
         const uint32_t jl = (uint32_t)(q0 + lane - pg * mp);
-        if (q0 + lane < c1) ld256<false>(a.in + 2 * (q0 + lane), n0, n1);
+        if (q0 + lane < c1) ld_pair<TEX>(a, q0 + lane, n0, n1);
         uint4 cr = make_uint4(0, 0, 0, 0);
         if (CBC && DEC && q0 % mp != 0) cr = a.in[2 * q0 - 1];  // out of place only (in place: q0 is a page start)
         const uint64_t q1 = q0 + unit < c1 ? q0 + unit : c1;  // the last unit may be partial
-        pair_stream<DEC, CBC>(a, cph, q0, q1, mp, cr, pg, jl, n0, n1);
+        pair_stream<DEC, CBC, TEX>(a, cph, q0, q1, mp, cr, pg, jl, n0, n1);
     }
 }
 
@@ -465,6 +480,8 @@ __device__ __forceinline__ Job job_of(const LaunchArgs &a) {
     j.n_pages = a.n_pages;
     j.m = a.m;
     j.in_place = a.in_place;
+    j.tex = a.tex_in;
+    j.tex_off = a.tex_off;
     return j;
 }
 
@@ -477,7 +494,7 @@ __device__ __forceinline__ Job job_of(const LaunchArgs &a) {
 #endif
 constexpr int kPairThreads = KG_PAIR_TPB;  // threads per CTA of the block-pair kernels
 
-template <int NR, int DIR, int MODE, bool PAIR>
+template <int NR, int DIR, int MODE, bool PAIR, bool TEX = false>
 __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
     constexpr bool DEC = (DIR == 1);
@@ -494,8 +511,8 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
 #endif
     const uint32_t lb = lane_bytes();
     if (PAIR) {
-        if (DEC) blockpair_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
-        else blockpair_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+        if (DEC) blockpair_body<true, CBC, TEX>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
+        else blockpair_body<false, CBC, TEX>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
     } else {
         if (DEC) blockpar_body<true, CBC>(job_of(a), ParamDec<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
         else blockpar_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
@@ -744,7 +761,7 @@ struct RegKeyPolicy {
 // Mixed-key block-pair kernel (m even): CBC decrypt, ECB both ways.
 // CONSTK: round keys from the constant bank (ConstKeyPolicy), else per-lane
 // __ldg from the device snapshot (KeyedPolicy).
-template <int NR, int DIR, int MODE, bool CONSTK>
+template <int NR, int DIR, int MODE, bool CONSTK, bool TEX = false>
 __global__ void __launch_bounds__(kPairThreads, 1) kg_keyed_pair(const __grid_constant__ LaunchArgs a, KeyedArgs k) {
     extern __shared__ __align__(16) char sm[];
     constexpr bool DEC = (DIR == 1);
@@ -754,7 +771,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) kg_keyed_pair(const __grid_co
     const uint32_t lb = lane_bytes();
     if (CONSTK) {
         const ConstKeyPolicy<NR, DEC> pol{sm, lb, k.key_ids, k.status, a.n_pages};
-        blockpair_body<DEC, CBC>(job_of(a), pol, blockIdx.x, gridDim.x);
+        blockpair_body<DEC, CBC, TEX>(job_of(a), pol, blockIdx.x, gridDim.x);
     } else {
         const KeyedPolicy<NR, DEC> pol{sm, lb, DEC ? k.tab->dec : k.tab->enc, k.tab->nr, k.key_ids, k.status, a.n_pages};
         blockpair_body<DEC, CBC>(job_of(a), pol, blockIdx.x, gridDim.x);
@@ -805,6 +822,9 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_blockpar<NR, 1, 0, true>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_blockpar<NR, 1, 1, true>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_blockpar<NR, 0, 1, true>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 0, true, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 1, 1, true, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_blockpar<NR, 0, 1, true, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, false>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed<NR, 1, 0>, kSmemDec)) != cudaSuccess) return e;
@@ -814,6 +834,9 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_keyed_pair<NR, 1, 0, true>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_pair<NR, 1, 1, true>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_pair<NR, 0, 1, true>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 1, 0, true, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 1, 1, true, true>, kSmemDec)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_pair<NR, 0, 1, true, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_pair<NR, 1, 0, false>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_pair<NR, 1, 1, false>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_pair<NR, 0, 1, false>, kSmemEnc)) != cudaSuccess) return e;
@@ -864,6 +887,11 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
         const char *e = getenv("KG_PAIR");
         return (e && *e == '0') ? 0 : 1;
     }();
+    if (pair_ok && (a.m & 1) == 0 && a.tex_in) {
+        if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_blockpar<NR, 1, 0, true, true>, grid, kPairThreads, kSmemDec, st, a);
+        if (dir == 1) return launch_pdl_tpb(kg_blockpar<NR, 1, 1, true, true>, grid, kPairThreads, kSmemDec, st, a);
+        return launch_pdl_tpb(kg_blockpar<NR, 0, 1, true, true>, grid, kPairThreads, kSmemEnc, st, a);
+    }
     if (pair_ok && (a.m & 1) == 0) {
         if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_blockpar<NR, 1, 0, true>, grid, kPairThreads, kSmemDec, st, a);
         if (dir == 1) return launch_pdl_tpb(kg_blockpar<NR, 1, 1, true>, grid, kPairThreads, kSmemDec, st, a);
@@ -900,6 +928,11 @@ cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedA
         return launch_pdl_tpb(kg_keyed_chain<NR, false>, grid, kPairThreads, kSmemEnc, st, a, k);
     }
     if (v > 0 && (a.m & 1) == 0) {
+        if (v == 2 && a.tex_in) {
+            if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 0, true, true>, grid, kPairThreads, kSmemDec, st, a, k);
+            if (dir == 1) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 1, true, true>, grid, kPairThreads, kSmemDec, st, a, k);
+            return launch_pdl_tpb(kg_keyed_pair<NR, 0, 1, true, true>, grid, kPairThreads, kSmemEnc, st, a, k);
+        }
         if (v == 2) {
             if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 0, true>, grid, kPairThreads, kSmemDec, st, a, k);
             if (dir == 1) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 1, true>, grid, kPairThreads, kSmemDec, st, a, k);

@@ -167,6 +167,18 @@ struct Ctx {
     uint32_t *status_dev = nullptr;
     bool status_busy[kStatusSlots] = {};
     uint32_t status_next = 0;
+    // 1D linear textures over kernel inputs (LaunchArgs::tex_in), LRU cache
+    struct TexEnt {
+        uintptr_t base = 0;
+        uint64_t bytes = 0;
+        cudaTextureObject_t tex = 0;
+        UseSet use;
+        uint64_t stamp = 0;
+    };
+    std::vector<TexEnt *> texs;
+    uint64_t tex_clock = 0;
+    uint64_t tex_max_elems = 0;   // cudaDevAttrMaxTexture1DLinearWidth (0: textures off)
+    uint64_t tex_align = 512;
     PFN_writeValue64 write_value64 = nullptr;
     PFN_waitValue64 wait_value64 = nullptr;
 };
@@ -246,7 +258,10 @@ cudaEvent_t take_event() {
     return e;
 }
 
+void tex_clear();
+
 void free_staging() {
+    tex_clear();  // cached textures may cover the slot buffers
     for (int i = 0; i < kMaxSlots; i++) {
         if (g.slots[i].data) cudaFree(g.slots[i].data);
         if (g.slots[i].ivs) cudaFree(g.slots[i].ivs);
@@ -324,12 +339,115 @@ int64_t new_ticket(cudaStream_t st) {
     return t;
 }
 
+// A texture over device memory [p, p + bytes) for a block-pair launch's input
+// (LaunchArgs::tex_in / tex_off), from an LRU cache of 64; *ent = the entry
+// whose use must be recorded after the launch (nullptr: plain loads).
+// KG_TEXIN=0 disables.  Entries are destroyed only after every stream that
+// used them is done.
+bool tex_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("KG_TEXIN");
+        return !(e && *e == '0');
+    }();
+    return on && g.tex_max_elems;
+}
+
+int tex_for(const void *p, uint64_t bytes, kg::LaunchArgs *a, Ctx::TexEnt **ent) {
+    *ent = nullptr;
+    if (!tex_enabled() || bytes == 0) return KG_OK;
+    const uintptr_t u = (uintptr_t)p, base = u & ~(uintptr_t)(g.tex_align - 1);
+    const uint64_t need = ((u - base) + bytes + 15) / 16 * 16;
+    if (need / 16 > g.tex_max_elems || need / 16 > (uint64_t)INT32_MAX) return KG_OK;
+    Ctx::TexEnt *hit = nullptr;
+    for (Ctx::TexEnt *e : g.texs)
+        if (e->base <= u && u + bytes <= e->base + e->bytes) {
+            hit = e;
+            break;
+        }
+    if (!hit) {
+        if (g.texs.size() >= 64) {  // evict the least recently used
+            size_t lru = 0;
+            for (size_t i = 1; i < g.texs.size(); i++)
+                if (g.texs[i]->stamp < g.texs[lru]->stamp) lru = i;
+            Ctx::TexEnt *e = g.texs[lru];
+            KG_CU(e->use.host_wait());
+            e->use.reset();
+            cudaDestroyTextureObject(e->tex);
+            delete e;
+            g.texs.erase(g.texs.begin() + lru);
+        }
+        cudaResourceDesc rd = {};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = (void *)base;
+        rd.res.linear.desc = cudaCreateChannelDesc<uint4>();
+        rd.res.linear.sizeInBytes = need;
+        cudaTextureDesc td = {};
+        td.readMode = cudaReadModeElementType;
+        cudaTextureObject_t t = 0;
+        if (cudaCreateTextureObject(&t, &rd, &td, nullptr) != cudaSuccess) {
+            cudaGetLastError();
+            return KG_OK;  // e.g. memory the texture unit cannot map: plain loads
+        }
+        hit = new Ctx::TexEnt;
+        hit->base = base;
+        hit->bytes = need;
+        hit->tex = t;
+        g.texs.push_back(hit);
+    }
+    hit->stamp = ++g.tex_clock;
+    a->tex_in = (unsigned long long)hit->tex;
+    a->tex_off = (int64_t)((u - hit->base) / 16);
+    *ent = hit;
+    return KG_OK;
+}
+
+void tex_clear() {
+    for (Ctx::TexEnt *e : g.texs) {
+        e->use.host_wait();
+        e->use.reset();
+        cudaDestroyTextureObject(e->tex);
+        delete e;
+    }
+    g.texs.clear();
+}
+
 int launch(int dir, int mode, int nr, const kg::LaunchArgs &a, cudaStream_t st) {
     // While the NSK holds some SMs, launched kernels use the others.
     const int sms = g.nsk.on ? g.num_sms - g.nsk.ctas : g.num_sms;
     cudaError_t e = kg::launch_pages(dir, mode, nr, a, sms > 0 ? sms : 1, st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_pages");
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    return KG_OK;
+}
+
+// A batch whose input is device memory read by the block-pair kernel: its page
+// loads go through a texture (tex_for).  A 1D linear texture holds at most
+// tex_max_elems texels, so larger batches (C5: 64 GiB) are launched as
+// page-aligned windows that fit one texture each (pages are independent).
+int launch_tex(int dir, int mode, int nr, kg::LaunchArgs a, uint32_t page_bytes, cudaStream_t st) {
+    const uint64_t total = a.n_pages * (uint64_t)page_bytes;
+    uint64_t win = a.n_pages;
+    if (tex_enabled()) {
+        uint64_t cap = g.tex_max_elems < (uint64_t)INT32_MAX ? g.tex_max_elems : (uint64_t)INT32_MAX;
+        cap = cap * 16 > g.tex_align ? cap * 16 - g.tex_align : 0;  // bytes, room for base alignment
+        if (total > cap) win = cap / page_bytes;
+    }
+    if (win == 0) win = a.n_pages;
+    const uint64_t n = a.n_pages;
+    for (uint64_t p = 0; p < n; p += win) {
+        kg::LaunchArgs w = a;
+        const uint64_t np = n - p < win ? n - p : win;
+        const uint64_t blk = p * (page_bytes / 16);
+        w.in = a.in + blk;
+        w.out = a.out + blk;
+        w.ivs = a.ivs ? a.ivs + p : nullptr;
+        w.n_pages = np;
+        Ctx::TexEnt *te = nullptr;
+        int rc = tex_for(w.in, np * page_bytes, &w, &te);
+        if (rc != KG_OK) return rc;
+        if ((rc = launch(dir, mode, nr, w, st)) != KG_OK) return rc;
+        if (te) KG_CU(te->use.record(st));
+    }
     return KG_OK;
 }
 
@@ -466,12 +584,19 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         if (keyed) {
             kg::KeyedArgs k = *keyed;
             k.key_ids += p0;
+            Ctx::TexEnt *te = nullptr;
+            if (kg::keyed_uses_const_keys(dir, mode, a.m) && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
             cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, g.num_sms, g.s_comp);
             if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
             g_launches.fetch_add(1, std::memory_order_relaxed);
+            if (te) KG_CU(te->use.record(g.s_comp));
         } else {
+            Ctx::TexEnt *te = nullptr;
+            const bool chain = (dir == KG_ENCRYPT && mode == KG_MODE_CBC);
+            if (!chain && (a.m & 1) == 0 && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
             rc = launch(dir, mode, nr, a, g.s_comp);
             if (rc != KG_OK) return rc;
+            if (te) KG_CU(te->use.record(g.s_comp));
         }
         KG_CU(cudaEventRecord(s.done, g.s_comp));
         trace(i, 'k', g.s_comp);
@@ -642,6 +767,8 @@ int kg_init(int device) {
     if (prop.major != 10) return KG_ENOTSUP;  // built for sm_100a only
     g.device = device;
     g.num_sms = prop.multiProcessorCount;
+    g.tex_max_elems = (uint64_t)prop.maxTexture1DLinear;
+    g.tex_align = prop.textureAlignment ? (uint64_t)prop.textureAlignment : 512;
     kg::BaseTables t;
     kg::build_base_tables(&t);
     KG_CU(kg::kernels_init(t));
@@ -900,7 +1027,8 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
         a.m = page_bytes / 16;
         a.in_place = (in == out);
         a.rk = rk;
-        rc = launch(dir, mode, ks.nr, a, st);
+        if (kin == K_DEVICE && !chain && (a.m & 1) == 0) rc = launch_tex(dir, mode, ks.nr, a, page_bytes, st);
+        else rc = launch(dir, mode, ks.nr, a, st);
     } else {
         rc = submit_staged(dir, mode, ks.nr, rk, (const uint8_t *)in, kin, (uint8_t *)out, kout, n_pages,
                            page_bytes, (const uint8_t *)ivs, kiv, st);
@@ -1060,9 +1188,12 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
         if (rc != KG_OK) return rc;
         KG_CU(g.ktab_used[g.ktab_cur].record(st));
     } else {
+        Ctx::TexEnt *te = nullptr;
+        if (ck && kin == K_DEVICE && (rc = tex_for(zin, total, &a, &te)) != KG_OK) return rc;
         cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, st);
         if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
         g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (te) KG_CU(te->use.record(st));
     }
     if (ck) KG_CU(g.ckeys_users.record(st));
     const int64_t t = new_ticket(st);
