@@ -111,6 +111,9 @@ cudaError_t launch_pages_keyed(int dir, int mode, int nr, const LaunchArgs &a, c
 // from the snapshot `tab` for direction `dir` before the launch.
 bool keyed_uses_const_keys(int dir, int mode, uint32_t m);
 cudaError_t load_const_keys(const DevKeyTable *tab, int dir, cudaStream_t st);
+// True if a keyed launch of this shape has a texture-pipe input variant
+// (LaunchArgs::tex_in honoured).
+bool keyed_takes_tex(int dir, int mode, uint32_t m);
 // Launch the NSK cooperatively with `ctas` CTAs; it expects request seq0 next
 // and exits after idle_ns without a posted request (or on a quit request).
 cudaError_t launch_nsk(NskRing *ring_dev, NskCtl *ctl, uint64_t seq0, uint64_t idle_ns, int ctas, cudaStream_t st);

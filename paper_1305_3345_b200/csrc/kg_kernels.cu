@@ -436,7 +436,7 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
 
 // ---- chain body: CBC encrypt, one thread per page chain ------------------------
 // WIDE (m even): blocks move two at a time with 256-bit loads/stores.
-template <bool WIDE, class Cipher>
+template <bool WIDE, class Cipher, bool TEX = false>
 __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
     const uint32_t m = a.m;
     const uint64_t p0 = part_start(a.n_pages, ncta, cta);
@@ -448,10 +448,15 @@ __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, ui
         const auto kl = cph.lane(p);
         if (WIDE) {
             uint4 x0, x1;
-            ld256<true>(src, x0, x1);
+            // TEX: page loads through the texture pipe (see ld_pair); pair index of block j = (p*m + j) / 2
+            if (TEX) ld_pair<true>(a, (p * m) >> 1, x0, x1);
+            else ld256<true>(src, x0, x1);
             for (uint32_t j = 0; j < m; j += 2) {
                 uint4 n0 = x0, n1 = x1;
-                if (j + 2 < m) ld256<true>(src + j + 2, n0, n1);  // prefetch P_{j+2}, P_{j+3}
+                if (j + 2 < m) {  // prefetch P_{j+2}, P_{j+3}
+                    if (TEX) ld_pair<true>(a, (p * m + j + 2) >> 1, n0, n1);
+                    else ld256<true>(src + j + 2, n0, n1);
+                }
                 // C_j = E_K(P_j ^ C_{j-1}); the first AddRoundKey folds into the same XOR
                 const uint4 c0 = cph.rounds(kl, cph.first(kl, xor4(x0, prev)));
                 prev = cph.rounds(kl, cph.first(kl, xor4(x1, c0)));
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
 #endif
 }
 
-template <int NR, bool WIDE>
+template <int NR, bool WIDE, bool TEX = false>
 __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
 #ifdef KG_CTA_STAMPS
@@ -543,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant_
     unsigned long long t_filled;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_filled));
 #endif
-    cbc_enc_body<WIDE>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
+    cbc_enc_body<WIDE, ParamEnc<NR>, TEX>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
 #ifdef KG_CTA_STAMPS
     unsigned long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -779,14 +784,14 @@ __global__ void __launch_bounds__(kPairThreads, 1) kg_keyed_pair(const __grid_co
 }
 
 // Mixed-key CBC encrypt: one chain per thread, the page's keys in registers.
-template <int NR, bool WIDE>
+template <int NR, bool WIDE, bool TEX = false>
 __global__ void __launch_bounds__(kPairThreads, 1) kg_keyed_chain(const __grid_constant__ LaunchArgs a, KeyedArgs k) {
     extern __shared__ __align__(16) char sm[];
     fill_tables<false>(sm);
     pdl_prologue_done();
     __syncthreads();
     const RegKeyPolicy<NR> pol{sm, lane_bytes(), k.tab->enc, k.tab->nr, k.key_ids, k.status, a.n_pages};
-    cbc_enc_body<WIDE>(job_of(a), pol, blockIdx.x, gridDim.x);
+    cbc_enc_body<WIDE, RegKeyPolicy<NR>, TEX>(job_of(a), pol, blockIdx.x, gridDim.x);
 }
 
 template <int NR, int DIR, int MODE>
@@ -827,6 +832,7 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_blockpar<NR, 0, 1, true, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_cbc_enc<NR, false>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_cbc_enc<NR, true, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed<NR, 1, 0>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed<NR, 1, 1>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed<NR, 0, 1>, kSmemEnc)) != cudaSuccess) return e;
@@ -842,6 +848,7 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_keyed_pair<NR, 0, 1, false>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_chain<NR, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_chain<NR, false>, kSmemEnc)) != cudaSuccess) return e;
+    if ((e = set_smem(kg_keyed_chain<NR, true, true>, kSmemEnc)) != cudaSuccess) return e;
     return cudaSuccess;
 }
 
@@ -876,6 +883,7 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     if (dir == 0 && mode == 0) {
         const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
+        if ((a.m & 1) == 0 && a.tex_in) return launch_pdl(kg_cbc_enc<NR, true, true>, grid, kSmemEnc, st, a);
         if ((a.m & 1) == 0) return launch_pdl(kg_cbc_enc<NR, true>, grid, kSmemEnc, st, a);
         return launch_pdl(kg_cbc_enc<NR, false>, grid, kSmemEnc, st, a);
     }    uint64_t want = (nb + 255) / 256;
@@ -924,6 +932,8 @@ cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedA
     const unsigned grid = (unsigned)want;
     const int v = keyed_variant();
     if (v > 0 && chain) {
+        if ((a.m & 1) == 0 && a.tex_in)
+            return launch_pdl_tpb(kg_keyed_chain<NR, true, true>, grid, kPairThreads, kSmemEnc, st, a, k);
         if ((a.m & 1) == 0) return launch_pdl_tpb(kg_keyed_chain<NR, true>, grid, kPairThreads, kSmemEnc, st, a, k);
         return launch_pdl_tpb(kg_keyed_chain<NR, false>, grid, kPairThreads, kSmemEnc, st, a, k);
     }
@@ -952,6 +962,10 @@ cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedA
 
 bool keyed_uses_const_keys(int dir, int mode, uint32_t m) {
     return keyed_variant() == 2 && !(dir == 0 && mode == 0) && (m & 1) == 0;
+}
+
+bool keyed_takes_tex(int dir, int mode, uint32_t m) {
+    return (m & 1) == 0 && ((dir == 0 && mode == 0) ? keyed_variant() > 0 : keyed_variant() == 2);
 }
 
 cudaError_t load_const_keys(const DevKeyTable *tab, int dir, cudaStream_t st) {

@@ -585,15 +585,14 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
             kg::KeyedArgs k = *keyed;
             k.key_ids += p0;
             Ctx::TexEnt *te = nullptr;
-            if (kg::keyed_uses_const_keys(dir, mode, a.m) && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
+            if (kg::keyed_takes_tex(dir, mode, a.m) && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
             cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, g.num_sms, g.s_comp);
             if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
             g_launches.fetch_add(1, std::memory_order_relaxed);
             if (te) KG_CU(te->use.record(g.s_comp));
         } else {
             Ctx::TexEnt *te = nullptr;
-            const bool chain = (dir == KG_ENCRYPT && mode == KG_MODE_CBC);
-            if (!chain && (a.m & 1) == 0 && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
+            if ((a.m & 1) == 0 && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
             rc = launch(dir, mode, nr, a, g.s_comp);
             if (rc != KG_OK) return rc;
             if (te) KG_CU(te->use.record(g.s_comp));
@@ -1027,7 +1026,7 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
         a.m = page_bytes / 16;
         a.in_place = (in == out);
         a.rk = rk;
-        if (kin == K_DEVICE && !chain && (a.m & 1) == 0) rc = launch_tex(dir, mode, ks.nr, a, page_bytes, st);
+        if (kin == K_DEVICE && (a.m & 1) == 0) rc = launch_tex(dir, mode, ks.nr, a, page_bytes, st);
         else rc = launch(dir, mode, ks.nr, a, st);
     } else {
         rc = submit_staged(dir, mode, ks.nr, rk, (const uint8_t *)in, kin, (uint8_t *)out, kout, n_pages,
@@ -1189,7 +1188,8 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
         KG_CU(g.ktab_used[g.ktab_cur].record(st));
     } else {
         Ctx::TexEnt *te = nullptr;
-        if (ck && kin == K_DEVICE && (rc = tex_for(zin, total, &a, &te)) != KG_OK) return rc;
+        if (kin == K_DEVICE && kg::keyed_takes_tex(dir, mode, a.m) && (rc = tex_for(zin, total, &a, &te)) != KG_OK)
+            return rc;
         cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, st);
         if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
         g_launches.fetch_add(1, std::memory_order_relaxed);
