@@ -154,13 +154,25 @@ KG_API int kg_shutdown(void);
 /* Static description of a status code; never NULL. */
 KG_API const char *kg_strerror(int status);
 
+/* Diagnostic environment switches (read once per process; defaults are the
+ * measured best, each alternative kept for A/B runs -- DESIGN.md):
+ *   KG_TEXIN=0       page loads by LDG instead of the texture pipe
+ *   KG_D2H_LAG=0|2   staged D2H not held back / only between equal chunks
+ *   KG_RAMP_DOWN=0..3  end-ramp levels of the staging schedule (default 3)
+ *   KG_KEYED=0|1     mixed-key kernels: one block per lane / __ldg round keys
+ *   KG_PAIR=0        one block per lane instead of block pairs
+ *   KG_PDL=0         no programmatic dependent launch
+ *   KG_TRACE=1       per-chunk staging timeline on stderr at kg_wait
+ *   KG_NSK_STAMPS=1  NSK per-request %globaltimer stamps;  KG_DEBUG=1 CUDA errors */
+
 /* Staging pipeline for batches touching host memory: chunk size in bytes
  * (rounded down to whole pages, at least one page; 0 = auto: 8 MiB, or
  * 16 MiB for CBC encryption, whose per-page chains need the longer copy to
  * hide behind) and number of device staging slots (2..8).  Takes effect for
- * later submits.  Defaults: auto, 4 slots (PAPER.md:437-440's "three buffers" plus one: the D2H of a chunk
- * is held back until the next chunk's H2D has landed, profiles/r1_pinned).  Environment overrides at
- * kg_init: KG_CHUNK_BYTES, KG_STAGING_SLOTS.  KG_EINVAL on bad values. */
+ * later submits.  Defaults: auto, 4 slots (PAPER.md:437-440's "three
+ * buffers" plus one: the D2H of a chunk is held back until the next chunk's
+ * H2D has landed, profiles/r1_lag).  Environment overrides at kg_init:
+ * KG_CHUNK_BYTES, KG_STAGING_SLOTS.  KG_EINVAL on bad values. */
 KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);
 
 /* How batches touching pinned host memory reach the GPU (rows a3/a8 vs f4):
