@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: the KG_PTEX variant was reverted after this A/B; see profiles/r1_tex/README.md)
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 O=gpurun_out/${1:-ptex}; mkdir -p $O
 KG_PTEX=1 timeout 1500 python -m pytest tests/test_parity_gpu.py tests/test_fuzz_gpu.py tests/test_fullsize_gpu.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
