@@ -767,6 +767,10 @@ int kg_init(int device) {
     g.device = device;
     g.num_sms = prop.multiProcessorCount;
     g.tex_max_elems = (uint64_t)prop.maxTexture1DLinear;
+    if (const char *e = getenv("KG_TEX_MAX_ELEMS")) {  // testing: smaller texture windows
+        unsigned long long v = strtoull(e, nullptr, 0);
+        if (v >= 1024 && v < g.tex_max_elems) g.tex_max_elems = v;
+    }
     g.tex_align = prop.textureAlignment ? (uint64_t)prop.textureAlignment : 512;
     kg::BaseTables t;
     kg::build_base_tables(&t);

@@ -223,3 +223,22 @@ def test_staged_d2h_lag_modes(lag):
                         "-k", "(staged_batches or small_staging or cbc_pinned or mixed_residency) and not lag_modes"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("env", [{"KG_TEXIN": "0"}, {"KG_TEX_MAX_ELEMS": "4096"}])
+def test_texture_path_variants(env):
+    """Device-batch parity with plain LDG page loads (KG_TEXIN=0) and with
+    64 KiB texture windows (KG_TEX_MAX_ELEMS=4096: every batch above 16 pages
+    runs as several windowed launches, in place and out of place, with IV
+    offsets), in a child process (both are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from gpu_util import kg_ready
+    kg_ready()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_parity_gpu.py"),
+                        "-k", "(cbc_device or ecb or tail_pool) and not texture_path"],
+                       cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
