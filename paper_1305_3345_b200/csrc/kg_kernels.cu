@@ -19,7 +19,9 @@
 //  * Block-parallel kernel (CBC decrypt, ECB both ways): each warp streams a
 //    contiguous range of blocks; with even blocks-per-page (the default) each
 //    lane owns two consecutive blocks (1 KiB per warp step, coalesced
-//    LDG.256/STG.256), else one (512 B, LDG.128).  The CBC predecessor C_{j-1}
+//    LDG.256/STG.256 -- or, for device-memory input, two texel fetches
+//    through the texture pipe, off the LSU data pipe the lookups saturate),
+//    else one (512 B, LDG.128).  The CBC predecessor C_{j-1}
 //    comes from the neighbouring lane by one rotate-SHFL (lane 0: the previous
 //    unit's lane 31, or the IV at a page start); the next unit's load is in
 //    flight while the current unit's rounds run.
