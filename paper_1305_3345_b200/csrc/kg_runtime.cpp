@@ -88,6 +88,11 @@ struct UseSet {
     cudaError_t record(cudaStream_t st) {
         for (auto &p : v)
             if (p.first == st) return cudaEventRecord(p.second, st);
+        if (v.size() >= 64) {  // many short-lived streams: fold the old uses into a host wait
+            cudaError_t r = host_wait();
+            if (r != cudaSuccess) return r;
+            reset();
+        }
         cudaEvent_t e;
         cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
         if (r != cudaSuccess) return r;
