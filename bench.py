@@ -370,9 +370,12 @@ def run_ours(args):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+        step_ms = []
         t0 = time.perf_counter()
         for _ in range(e_steps):
+            ts = time.perf_counter()
             kg.wait(kg.submit_pages(direction, kg.MODE_CBC, hx, hout, n, PB, hiv, 0, stream))
+            step_ms.append((time.perf_counter() - ts) * 1e3)
         te = time.perf_counter() - t0
         if dist:
             tt = torch.tensor([te], dtype=torch.float64, device=red_dev)
@@ -381,7 +384,9 @@ def run_ours(args):
         total_e2e = (n_total * PB if scaling == "strong" else bytes_step * world) * e_steps
         e2e = {"value": total_e2e / te / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": bytes_step + 16 * n, "d2h_bytes_per_step": bytes_step,
-               "steps": e_steps, "residency": residency}
+               "steps": e_steps, "residency": residency,
+               "step_ms_min_median_max": [round(min(step_ms), 3), round(sorted(step_ms)[len(step_ms) // 2], 3),
+                                          round(max(step_ms), 3)]}
         # host-link roofline for this path: pinned H2D and D2H copy engines at once
         link = duplex_link_gbs(torch, hx, hout)
         e2e["link_duplex_gbs_per_direction"] = link
@@ -450,7 +455,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--step-events", action="store_true",
                     help="record a CUDA event pair around every step (serialises programmatic dependent launch)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -25,13 +25,16 @@ def main(chunk_mib=16, slots=3, k=10, direction=1, key_bytes=16, mib=256):
     for _ in range(3):
         kg.wait(kg.submit_pages(direction, 0, hx, ho, n, 4096, hiv, 0))
     torch.cuda.synchronize()
+    steps = []
     t0 = time.perf_counter()
     for _ in range(k):
+        ts = time.perf_counter()
         kg.wait(kg.submit_pages(direction, 0, hx, ho, n, 4096, hiv, 0))
+        steps.append(round((time.perf_counter() - ts) * 1e3, 3))
     t = (time.perf_counter() - t0) / k
     print(json.dumps({"test": "staged_ab", "pdl": os.environ.get("KG_PDL", "1"), "chunk_mib": chunk_mib,
                       "slots": slots, "dir": direction, "key_bytes": key_bytes, "mib": mib,
-                      "gbs": n * 4096 / t / 1e9}), flush=True)
+                      "gbs": n * 4096 / t / 1e9, "step_ms": steps}), flush=True)
 
 
 if __name__ == "__main__":
