@@ -242,3 +242,33 @@ def test_texture_path_variants(env):
                         "-k", "(cbc_device or ecb or tail_pool) and not texture_path"],
                        cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_texture_cache_eviction_many_buffers_and_streams():
+    """More distinct input buffers (80) than the texture cache holds (64) and
+    more streams (70) than a use set tracks (64): entries are evicted only
+    after their launches finish, and every batch still matches the oracle."""
+    from gpu_util import kg_ready
+    kg, torch = kg_ready()
+    n, pb = 3, 4096
+    key = synth.make_key(16, seed=808)
+    kg.set_key(0, key)
+    streams = [torch.cuda.Stream() for _ in range(70)]
+    jobs = []
+    for b in range(80):
+        data = synth.make_pages(n, pb, seed=900 + b)
+        ivs = synth.make_ivs(n, seed=1000 + b)
+        x = torch.from_numpy(data).cuda()
+        iv = torch.from_numpy(ivs).cuda()
+        out = torch.empty_like(x)
+        torch.cuda.synchronize()
+        s = streams[b % len(streams)]
+        jobs.append((kg.submit_pages(1, 0, x, out, n, pb, iv, 0, s), data, ivs, x, iv, out))
+        if b % 7 == 6:                      # some buffers freed and reallocated while others are in flight
+            t, d, v, *_ = jobs.pop(0)
+            kg.wait(t)
+    for t, data, ivs, x, iv, out in jobs:
+        kg.wait(t)
+        torch.cuda.synchronize()
+        exp = oracle_pages(1, 0, key, data, n, pb, ivs)
+        assert first_mismatch(out.cpu().numpy(), exp) is None
