@@ -39,13 +39,23 @@ build/kgpu_crypt: examples/kgpu_crypt.c include/kg.h $(LIB) | build
 	gcc -std=c99 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lkgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 # diagnostics (not part of `all`): copy-engine overlap, per-CTA stamps, bitsliced round
-tools: build/copy_overlap build/cta_stamps build/bitslice_bench build/soak_tsan
+tools: build/copy_overlap build/cta_stamps build/bitslice_bench build/soak_tsan build/pipes_tex build/pipes_lds build/pipes_ldpath \
+       build/hybrid_bench build/pipe_variants
 
 build/copy_overlap: tools/copy_overlap.cu | build
 	$(NVCC) -O2 $(ARCH) -o $@ $<
 
 build/cta_stamps: tools/cta_stamps.cu $(CSRC)/kg_kernels.cu $(CSRC)/kg_tables.cpp $(wildcard $(CSRC)/*.cuh) | build
 	$(NVCC) -O3 -std=c++17 $(ARCH) -o $@ $< $(CSRC)/kg_tables.cpp
+
+build/pipes_tex build/pipes_lds build/pipes_ldpath: build/%: tools/%.cu | build
+	$(NVCC) -O3 -std=c++17 $(ARCH) -o $@ $<
+
+build/hybrid_bench: tools/hybrid_bench.cu tools/kg_sbox_bs.cuh | build
+	$(NVCC) -O3 -std=c++17 $(ARCH) -Itools -o $@ $<
+
+build/pipe_variants: tools/pipe_variants.cu | build
+	$(NVCC) -O2 -std=c++17 $(ARCH) -o $@ $< -lcuda
 
 build/bitslice_bench: tools/bitslice_bench.cu tools/kg_sbox_bs.cuh | build
 	$(NVCC) -O3 -std=c++17 $(ARCH) -o $@ $<
