@@ -1,6 +1,8 @@
 """Randomised parity sweep: random (direction, mode, key size, page count,
 page size, residency, in-place, host path) cases, each compared byte for byte
 with the oracle.  Sizes stay small so the oracle finishes quickly."""
+import os
+
 import numpy as np
 import pytest
 
@@ -12,8 +14,9 @@ pytestmark = pytest.mark.gpu
 
 def test_random_cases():
     kg, torch = kg_ready()
-    rng = np.random.default_rng(20261017)
-    for case in range(150):
+    # KG_FUZZ_CASES / KG_FUZZ_SEED: longer soak runs (tools/gpu_fuzz_soak.sh)
+    rng = np.random.default_rng(int(os.environ.get("KG_FUZZ_SEED", "20261017")))
+    for case in range(int(os.environ.get("KG_FUZZ_CASES", "150"))):
         d = int(rng.integers(0, 2))
         mode = int(rng.integers(0, 2))
         kb = int(rng.choice([16, 24, 32]))
