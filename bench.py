@@ -420,6 +420,7 @@ def run_ours(args):
                    else "kg_blockpar" if (direction == 1 or mode == kg.MODE_ECB) else "kg_cbc_enc") + f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>",
         "algorithmic_bytes_per_launch": bytes_launch,
         "launches_per_step": launches_per_step,
+        "page_loads": "LDG" if os.environ.get("KG_TEXIN") == "0" else "texture pipe (TLD)",
     }
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
