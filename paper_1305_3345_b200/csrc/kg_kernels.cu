@@ -338,40 +338,58 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
 // that of its second block is its own first block.  A pair never straddles a
 // page (m even, ranges in whole pairs).
 
-// Stream the pairs [w0, w1) of one warp.  (n0, n1) holds the warp's first
-// unit (already loaded); carry = C of the block before w0 (if not a page start).
-template <bool DEC, bool CBC, bool TEX, class Cipher>
-__device__ __forceinline__ void pair_stream(const Job &a, const Cipher &cph, uint64_t w0, uint64_t w1, uint64_t mp,
-                                            uint4 carry, uint64_t page, uint32_t jp, uint4 n0, uint4 n1) {
+// G-block groups (G = 2: the block pairs above; G = 4, quads, was measured
+// 10% slower -- 126 registers, profiles/r1_tex/quad -- and is not instantiated).
+// A lane owns blocks G*q .. G*q+G-1 of group q; a warp unit is 32 groups.
+// The CBC predecessor of the lane's first block is the previous lane's last
+// block (one 4-word SHFL per unit), those of its other blocks are its own.
+template <int G, bool TEX>
+__device__ __forceinline__ void ld_group(const Job &a, uint64_t q, uint4 (&x)[G]) {
+#pragma unroll
+    for (int h = 0; h < G / 2; ++h) ld_pair<TEX>(a, (uint64_t)(G / 2) * q + h, x[2 * h], x[2 * h + 1]);
+}
+
+// Stream the groups [w0, w1) of one warp.  nx holds the warp's first unit
+// (already loaded); carry = C of the block before w0 (if not a page start).
+template <int G, bool DEC, bool CBC, bool TEX, class Cipher>
+__device__ __forceinline__ void group_stream(const Job &a, const Cipher &cph, uint64_t w0, uint64_t w1, uint64_t mg,
+                                             uint4 carry, uint64_t page, uint32_t jg, uint4 (&nx)[G]) {
     const uint32_t lane = threadIdx.x & 31;
     for (uint64_t u = w0; u < w1; u += 32) {
         const uint64_t q = u + lane;
         const bool act = q < w1;
-        const uint4 x0 = n0, x1 = n1;
-        if (q + 32 < w1) ld_pair<TEX>(a, q + 32, n0, n1);
+        uint4 x[G];
+#pragma unroll
+        for (int b = 0; b < G; ++b) x[b] = nx[b];
+        if (q + 32 < w1) ld_group<G, TEX>(a, q + 32, nx);
         uint4 prev = make_uint4(0, 0, 0, 0);
         if (CBC && DEC) {
-            const uint4 r = shfl4(x1, (lane + 31) & 31);
+            const uint4 r = shfl4(x[G - 1], (lane + 31) & 31);
             prev = (lane == 0) ? carry : r;
             carry = r;
-            if (act && jp == 0) prev = a.ivs[page];
+            if (act && jg == 0) prev = a.ivs[page];
         }
         const auto kl = cph.lane(page);
-        uint4 o0 = cph.rounds(kl, cph.first(kl, x0));
-        uint4 o1 = cph.rounds(kl, cph.first(kl, x1));
+        uint4 o[G];
+#pragma unroll
+        for (int b = 0; b < G; ++b) o[b] = cph.rounds(kl, cph.first(kl, x[b]));
         if (CBC && DEC) {
-            o0 = xor4(o0, prev);
-            o1 = xor4(o1, x0);
+            o[0] = xor4(o[0], prev);
+#pragma unroll
+            for (int b = 1; b < G; ++b) o[b] = xor4(o[b], x[b - 1]);
         }
-        if (act) st256<false>(a.out + 2 * q, o0, o1);
-        jp += 32;
-        if (jp >= mp) {
-            if (mp >= 32) {
-                jp -= (uint32_t)mp;
+        if (act) {
+#pragma unroll
+            for (int h = 0; h < G / 2; ++h) st256<false>(a.out + G * q + 2 * h, o[2 * h], o[2 * h + 1]);
+        }
+        jg += 32;
+        if (jg >= mg) {
+            if (mg >= 32) {
+                jg -= (uint32_t)mg;
                 ++page;
             } else {
-                page += jp / (uint32_t)mp;
-                jp %= (uint32_t)mp;
+                page += jg / (uint32_t)mg;
+                jg %= (uint32_t)mg;
             }
         }
     }
@@ -381,59 +399,66 @@ __device__ __forceinline__ void pair_stream(const Job &a, const Cipher &cph, uin
 // progress the 32 warps of a CTA evenly -- with equal static shares the last
 // warp finished ~16 us (5%) after the first (profiles/r1_tail).  So only the
 // first 15/16 of a CTA's pages are split statically; the rest is a pool that
-// warps drain once their static share is done: 64-block units out of place
+// warps drain once their static share is done: 32-group units out of place
 // (the unit's CBC predecessor is re-read from `in`, which nobody writes),
 // whole pages in place (the IV starts each page, so no predecessor crosses
 // warps).
-template <bool DEC, bool CBC, bool TEX = false, class Cipher>
-__device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
+template <int G, bool DEC, bool CBC, bool TEX, class Cipher>
+__device__ __forceinline__ void blockgroup_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
     __shared__ unsigned long long pool_next;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const uint64_t mp = a.m >> 1;  // pairs per page
-    const bool pool = mp >= 32 && a.n_pages >= 64ull * ncta;
-    uint64_t c0, c1, cmid;         // CTA range in pairs; the pool is [cmid, c1)
+    const uint64_t mg = a.m / G;  // groups per page
+    const bool pool = mg >= 32 && a.n_pages >= 64ull * ncta;
+    uint64_t c0, c1, cmid;        // CTA range in groups; the pool is [cmid, c1)
     if (pool || a.in_place) {
         const uint64_t P0 = part_start(a.n_pages, ncta, cta), P1 = part_start(a.n_pages, ncta, cta + 1);
-        c0 = P0 * mp;
-        c1 = P1 * mp;
-        cmid = pool ? (P1 - (P1 - P0) / KG_POOL_DIV) * mp : c1;
+        c0 = P0 * mg;
+        c1 = P1 * mg;
+        cmid = pool ? (P1 - (P1 - P0) / KG_POOL_DIV) * mg : c1;
         if (threadIdx.x == 0) pool_next = cmid;
     } else {
-        const uint64_t np = a.n_pages * mp;
-        c0 = part_start(np, ncta, cta);
-        c1 = part_start(np, ncta, cta + 1);
+        const uint64_t ng = a.n_pages * mg;
+        c0 = part_start(ng, ncta, cta);
+        c1 = part_start(ng, ncta, cta + 1);
         cmid = c1;
     }
     const uint64_t w0 = c0 + part_start(cmid - c0, nwarps, warp);
     const uint64_t w1 = c0 + part_start(cmid - c0, nwarps, warp + 1);
-    uint64_t page = (w0 + lane) / mp;
-    uint32_t jp = (uint32_t)((w0 + lane) - page * mp);  // pair index in the page
+    uint64_t page = (w0 + lane) / mg;
+    uint32_t jg = (uint32_t)((w0 + lane) - page * mg);  // group index in the page
 
     uint4 carry = make_uint4(0, 0, 0, 0);
     if (CBC && DEC) {
-        if (w0 < w1 && (w0 % mp) != 0) carry = a.in[2 * w0 - 1];
+        if (w0 < w1 && (w0 % mg) != 0) carry = a.in[G * w0 - 1];
     }
-    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-    if (w0 + lane < w1) ld_pair<TEX>(a, w0 + lane, n0, n1);
+    uint4 nx[G];
+#pragma unroll
+    for (int b = 0; b < G; ++b) nx[b] = make_uint4(0, 0, 0, 0);
+    if (w0 + lane < w1) ld_group<G, TEX>(a, w0 + lane, nx);
     __syncthreads();
-    pair_stream<DEC, CBC, TEX>(a, cph, w0, w1, mp, carry, page, jp, n0, n1);
+    group_stream<G, DEC, CBC, TEX>(a, cph, w0, w1, mg, carry, page, jg, nx);
     if (!pool) return;
-    const uint64_t unit = a.in_place ? mp : 32;  // pairs per claim
+    const uint64_t unit = a.in_place ? mg : 32;  // groups per claim
     for (;;) {
         unsigned long long q0 = 0;
         if (lane == 0) q0 = atomicAdd(&pool_next, (unsigned long long)unit);
         q0 = __shfl_sync(0xffffffffu, q0, 0);
         if (q0 >= c1) break;
-        // per-lane page / pair index (a 32-pair unit may cross a page boundary
-        // when mp is not a multiple of 32)
-        const uint64_t pg = (q0 + lane) / mp;
-        const uint32_t jl = (uint32_t)(q0 + lane - pg * mp);
-        if (q0 + lane < c1) ld_pair<TEX>(a, q0 + lane, n0, n1);
+        // per-lane page / group index (a 32-group unit may cross a page boundary
+        // when mg is not a multiple of 32)
+        const uint64_t pg = (q0 + lane) / mg;
+        const uint32_t jl = (uint32_t)(q0 + lane - pg * mg);
+        if (q0 + lane < c1) ld_group<G, TEX>(a, q0 + lane, nx);
         uint4 cr = make_uint4(0, 0, 0, 0);
-        if (CBC && DEC && q0 % mp != 0) cr = a.in[2 * q0 - 1];  // out of place only (in place: q0 is a page start)
+        if (CBC && DEC && q0 % mg != 0) cr = a.in[G * q0 - 1];  // out of place only (in place: q0 is a page start)
         const uint64_t q1 = q0 + unit < c1 ? q0 + unit : c1;  // the last unit may be partial
-        pair_stream<DEC, CBC, TEX>(a, cph, q0, q1, mp, cr, pg, jl, n0, n1);
+        group_stream<G, DEC, CBC, TEX>(a, cph, q0, q1, mg, cr, pg, jl, nx);
     }
+}
+
+template <bool DEC, bool CBC, bool TEX = false, class Cipher>
+__device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
+    blockgroup_body<2, DEC, CBC, TEX>(a, cph, cta, ncta);
 }
 
 // ---- chain body: CBC encrypt, one thread per page chain ------------------------
