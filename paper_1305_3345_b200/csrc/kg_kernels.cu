@@ -561,8 +561,13 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
 #endif
 }
 
+#ifndef KG_CHAIN_TPB
+#define KG_CHAIN_TPB 1024
+#endif
+constexpr int kChainThreads = KG_CHAIN_TPB;  // threads per CTA of the CBC-encrypt chain kernel
+
 template <int NR, bool WIDE, bool TEX = false>
-__global__ void __launch_bounds__(kThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
+__global__ void __launch_bounds__(kChainThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
 #ifdef KG_CTA_STAMPS
     unsigned long long t_start;
@@ -910,9 +915,10 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     if (dir == 0 && mode == 0) {
         const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
-        if ((a.m & 1) == 0 && a.tex_in) return launch_pdl(kg_cbc_enc<NR, true, true>, grid, kSmemEnc, st, a);
-        if ((a.m & 1) == 0) return launch_pdl(kg_cbc_enc<NR, true>, grid, kSmemEnc, st, a);
-        return launch_pdl(kg_cbc_enc<NR, false>, grid, kSmemEnc, st, a);
+        if ((a.m & 1) == 0 && a.tex_in)
+            return launch_pdl_tpb(kg_cbc_enc<NR, true, true>, grid, kChainThreads, kSmemEnc, st, a);
+        if ((a.m & 1) == 0) return launch_pdl_tpb(kg_cbc_enc<NR, true>, grid, kChainThreads, kSmemEnc, st, a);
+        return launch_pdl_tpb(kg_cbc_enc<NR, false>, grid, kChainThreads, kSmemEnc, st, a);
     }    uint64_t want = (nb + 255) / 256;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
