@@ -129,8 +129,8 @@ KG_API int64_t kg_submit_pages(int dir, int mode, const void *in, void *out,
  * as in kg_submit_pages (zero-copy, or the staging pipeline with each
  * chunk's launch reading its slice of key_ids).  A page naming an unset key or a key of another size makes
  * kg_wait return KG_ENOKEY (that page's output is unspecified).
- * Errors: as kg_submit_pages, plus KG_EINVAL for bad key_bytes or key_ids,
- * KG_ENOTSUP while the NSK runs. */
+ * Errors: as kg_submit_pages, plus KG_EINVAL for bad key_bytes or key_ids.
+ * While the NSK runs, keyed batches are launched on the SMs it leaves free. */
 KG_API int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out,
                                      uint64_t n_pages, uint32_t page_bytes,
                                      const void *ivs, const uint16_t *key_ids, int key_bytes,

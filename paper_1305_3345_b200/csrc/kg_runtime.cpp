@@ -591,7 +591,8 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
             k.key_ids += p0;
             Ctx::TexEnt *te = nullptr;
             if (kg::keyed_takes_tex(dir, mode, a.m) && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
-            cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, g.num_sms, g.s_comp);
+            const int sms = g.nsk.on ? (g.num_sms - g.nsk.ctas > 0 ? g.num_sms - g.nsk.ctas : 1) : g.num_sms;
+            cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, g.s_comp);
             if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
             g_launches.fetch_add(1, std::memory_order_relaxed);
             if (te) KG_CU(te->use.record(g.s_comp));
@@ -1129,7 +1130,6 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
     if (in != out && overlap((uintptr_t)in, total, (uintptr_t)out, total)) return KG_EINVAL;
     if (need_iv && overlap((uintptr_t)ivs, 16 * n_pages, (uintptr_t)out, total)) return KG_EINVAL;
     if (overlap((uintptr_t)key_ids, 2 * n_pages, (uintptr_t)out, total)) return KG_EINVAL;
-    if (g.nsk.on) return KG_ENOTSUP;  // the NSK owns SMs; keyed batches use launches only
     const void *zin = in, *zout = out, *ziv = ivs, *zid = key_ids;
     const Kind kin = classify(in, &zin), kout = classify(out, &zout), kid = classify(key_ids, &zid),
                kiv = need_iv ? classify(ivs, &ziv) : K_DEVICE;
@@ -1176,7 +1176,9 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
     k.tab = tab;
     k.status = g.status_dev + sslot;
     const int nr = key_bytes / 4 + 6;
-    const int sms = g.num_sms;
+    // keyed batches always launch; while the NSK holds SMs they use the others
+    // (a grid wider than the free SMs would wait behind the resident NSK forever)
+    const int sms = g.nsk.on ? (g.num_sms - g.nsk.ctas > 0 ? g.num_sms - g.nsk.ctas : 1) : g.num_sms;
     const bool ck = kg::keyed_uses_const_keys(dir, mode, a.m);
     if (ck && (g.ckeys_version != g.ktab_dev_version[g.ktab_cur] || g.ckeys_dir != dir)) {
         // refill the constant-bank copy behind every launch still reading it

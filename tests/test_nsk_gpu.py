@@ -205,3 +205,33 @@ def test_nsk_multithreaded_soak(nsk):
         t.join()
     assert not errors, errors[:5]
     assert len(seen) == len(set(seen)) == 1200
+
+
+@pytest.mark.parametrize("where", ["device", "pinned"])
+def test_keyed_batches_while_nsk_runs(nsk, where):
+    """Mixed-key batches are launched on the SMs the NSK leaves free (a grid
+    over all SMs would wait behind the resident NSK forever)."""
+    kg, torch = nsk
+    kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+    keys = {kid: synth.make_key(16, seed=300 + kid) for kid in (5, 6, 7)}
+    for kid, k in keys.items():
+        kg.set_key(kid, k)
+    s = torch.cuda.Stream()
+    for d, mode, n in ((1, 0, 3000), (0, 0, 700), (0, 1, 9000)):
+        rng = np.random.default_rng(n)
+        ids = np.array(list(keys), dtype=np.uint16)[rng.integers(0, 3, n)]
+        data = synth.make_pages(n, 4096, seed=n + 3)
+        ivs = synth.make_ivs(n, seed=n + 4) if mode == 0 else None
+        exp = np.empty_like(data)
+        for p in range(n):
+            sl = slice(p * 4096, (p + 1) * 4096)
+            exp[sl] = oracle_pages(d, mode, keys[int(ids[p])], data[sl], 1, 4096,
+                                   None if ivs is None else ivs[16 * p:16 * p + 16])
+        tin = put(torch, data, where)
+        tout = torch.empty_like(tin) if where == "device" else torch.empty_like(tin).pin_memory()
+        tiv = None if ivs is None else put(torch, ivs, where)
+        tid = torch.from_numpy(ids.astype(np.int16)).cuda()
+        s.synchronize()
+        kg.wait(kg.submit_pages_keyed(d, mode, tin, tout, n, 4096, tiv, tid, 16, s))
+        s.synchronize()
+        assert first_mismatch(tout.cpu().numpy(), exp) is None, (d, mode, n)
