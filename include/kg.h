@@ -159,7 +159,8 @@ KG_API const char *kg_strerror(int status);
  *   KG_TEXIN=0       page loads by LDG instead of the texture pipe
  *   KG_TEX_MAX_ELEMS=n  texture window limit in texels (testing the windowed
  *                    launches of batches larger than one texture, 2^28 texels)
- *   KG_D2H_LAG=0|2   staged D2H not held back / only between equal chunks
+ *   KG_D2H_LAG=0|2|3 staged D2H not held back / only between equal chunks /
+ *                    not for the last two chunks
  *   KG_RAMP_DOWN=0..3  end-ramp levels of the staging schedule (default 3)
  *   KG_KEYED=0|1     mixed-key kernels: one block per lane / __ldg round keys
  *   KG_PAIR=0        one block per lane instead of block pairs

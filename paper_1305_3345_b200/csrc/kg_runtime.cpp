@@ -540,14 +540,16 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     // compute time was added to the link time (profiles/r1_pinned/README.md,
     // "lagged_d2h": the H2D stream back at the contended link rate).
     // KG_D2H_LAG: 0 = off, 1 (default) = every chunk, 2 = only when the next
-    // chunk has the same size (measured: 1 and 2 within noise, 0 -4%)
+    // chunk has the same size, 3 = every chunk but the last two (the final
+    // D2Hs then overlap the final H2D instead of draining alone)
     static const int lag_mode = [] {
         const char *e = getenv("KG_D2H_LAG");
-        return (e && *e >= '0' && *e <= '2') ? *e - '0' : 1;
+        return (e && *e >= '0' && *e <= '3') ? *e - '0' : 1;
     }();
     const bool lag = lag_mode != 0;
     auto lag_on = [&](uint64_t j) {
-        return lag && j + 1 < sched.size() && (lag_mode == 1 || sched[j + 1] == sched[j]);
+        return lag && j + 1 < sched.size() && (lag_mode == 1 || (lag_mode == 2 && sched[j + 1] == sched[j]) ||
+                                               (lag_mode == 3 && j + 2 < sched.size()));
     };
     auto d2h = [&](uint64_t j, uint64_t pj) -> int {  // D2H stage of chunk j (first page pj)
         Slot &s = g.slots[j % (uint64_t)g.n_slots];
