@@ -415,6 +415,8 @@ def run_ours(args):
         "peak_basis": f"{SM_COUNT} SMs x {sm_max:.0f} MHz (sm_max) x {LDS_LANES_PER_CLK} lane-lookups/clk/SM / (16*Nr lookups per 16 B)",
         "frac_at_measured_clock": (achieved / compute_peak_gbs(key_bytes, clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
         "hbm_payload_peak": peaks["hbm_gbs"] / (2 + 16.0 / PB),
+        "hbm_peak_source": ("fallback 6650 GB/s (no MEASURED_PEAKS.json)" if peaks.get("_fallback")
+                            else "MEASURED_PEAKS.json"),
         "hbm_frac": achieved / (peaks["hbm_gbs"] / (2 + 16.0 / PB)),
         "kernel": (("kg_keyed_chain" if (direction == 0 and mode == kg.MODE_CBC) else "kg_keyed_pair") if keyed
                    else "kg_blockpar" if (direction == 1 or mode == kg.MODE_ECB) else "kg_cbc_enc") + f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>",
