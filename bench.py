@@ -371,6 +371,36 @@ def run_ours(args):
     value = total_bytes / elapsed / 1e9
     clocks = clk.summary()
 
+    # correctness check outside the timed region (every rank, SUM over ranks):
+    # one more step, then S sampled output pages go back through the inverse
+    # operation on the GPU and must reproduce the step's input pages.
+    check = None
+    if not args.no_check:
+        S = min(n, 1024)
+        gen = torch.Generator().manual_seed(1305 + rank)
+        idx = torch.randperm(n, generator=gen)[:S].sort().values.cuda()
+        xv = x.view(n, PB)
+        before = xv[idx].clone()
+        kg.wait(step())
+        torch.cuda.synchronize()
+        after = out.view(n, PB)[idx].contiguous()
+        iv_s = ivs.view(n, 16)[idx].contiguous().view(-1) if mode == kg.MODE_CBC else None
+        back = torch.empty_like(after)
+        inv = 1 - direction
+        if keyed:
+            kid_s = key_ids[idx].contiguous()
+            kg.wait(kg.submit_pages_keyed(inv, mode, after.view(-1), back.view(-1), S, PB, iv_s, kid_s, key_bytes, stream))
+        else:
+            kg.wait(kg.submit_pages(inv, mode, after.view(-1), back.view(-1), S, PB, iv_s, 0, stream))
+        torch.cuda.synchronize()
+        bad = torch.tensor([float((back != before).any(dim=1).sum()), float(S)], dtype=torch.float64, device=red_dev
+                           if dist else "cpu")
+        if dist:
+            dist.all_reduce(bad, op=dist.ReduceOp.SUM)
+        check = {"sampled_pages": int(bad[1]), "mismatched_pages": int(bad[0]),
+                 "method": "one extra step; sampled output pages through the inverse operation on the GPU "
+                           "must give back the step's input pages (parity vs the oracle: tests/)"}
+
     # secondary: e2e through the C ABI with pinned HOST buffers (H2D + compute + D2H timed)
     e2e = None
     if args.workload in ("c2", "c3", "c5") and not args.no_e2e:
@@ -460,6 +490,7 @@ def run_ours(args):
         "roofline": roof,
         "e2e": e2e,
         "gpu_launches": launches,
+        "check": check,
         "clocks": clocks,
         "wall_s_timed": t_wall,
     }
@@ -487,6 +518,7 @@ def main():
                     help="record a CUDA event pair around every step (serialises programmatic dependent launch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=0.0,
                     help="reference arm: oracle seconds per step (default: sized so the run takes ~2.5 min)")
