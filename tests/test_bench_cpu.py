@@ -33,3 +33,20 @@ def test_compute_peak_formula():
     # 148 SMs x 1965 MHz x 32 lookups/clk / 160 lookups per 16 B block (AES-128)
     assert abs(bench.compute_peak_gbs(16, 1965.0) - 930.624) < 1e-6
     assert abs(bench.compute_peak_gbs(32, 1965.0) - 664.7314285714286) < 1e-6
+
+
+def test_load_peaks_tolerates_key_names(tmp_path, monkeypatch):
+    """MEASURED_PEAKS.json is driver-written: bench.py reads the HBM copy
+    bandwidth and the max SM clock whatever the exact key names, and falls
+    back (never crashes) when it cannot find them."""
+    sys.path.insert(0, ROOT)
+    import bench
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    assert bench.load_peaks()["_fallback"] is True                       # no file
+    (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps({"hbm_copy_gbs": 6545.9, "sm_clock_max_mhz": 1965}))
+    p = bench.load_peaks()
+    assert p["hbm_gbs"] == 6545.9 and p["sm_max_mhz"] == 1965.0 and "_fallback" not in p
+    (tmp_path / "MEASURED_PEAKS.json").write_text("{not json")
+    assert bench.load_peaks()["_fallback"] is True
+    (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps({"something": 1}))
+    assert bench.load_peaks()["_fallback"] is True
