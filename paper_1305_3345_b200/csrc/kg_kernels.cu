@@ -164,7 +164,7 @@ __device__ __forceinline__ void st_stream(uint4 *p, uint4 v) { __stcs(p, v); }
 // 256-bit (two-block) global access: LDG.E.ENL2.256 / STG.E.ENL2.256 on
 // sm_100.  One L1 wavefront moves two blocks.  NOALLOC: L1::no_allocate --
 // measured +3.6% on the per-thread page-chain loads of the CBC-encrypt kernel
-// (profiles/r1m), -1.1% on the warp-coalesced decrypt loads, so the chain
+// (profiles/r1_ldst), -1.1% on the warp-coalesced decrypt loads, so the chain
 // kernel uses it and the block-pair kernel does not.  Same for the stores:
 // no_allocate +3.7% on CBC encrypt (568 -> 589 GB/s), -1.1% on decrypt.
 template <bool NOALLOC>

@@ -151,7 +151,7 @@ struct Ctx {
     cudaEvent_t iv_free[2] = {nullptr, nullptr};
     int iv_next = 0;
     int host_path = KG_HOST_AUTO;
-    uint64_t zc_max_bytes = 32ull << 20;  // zero-copy beats staging up to 32 MiB (tools/sweep.py, r1p)
+    uint64_t zc_max_bytes = 32ull << 20;  // zero-copy beats staging up to 32 MiB (tools/sweep.py; profiles/r1_pinned, r1_final8/sweep.jsonl)
     Nsk nsk;
     // mixed-key batches: host mirror of the key table, device snapshot ring,
     // pinned status words
