@@ -51,9 +51,11 @@ WORKLOADS = {
     "ecb_enc": (65536, 16, 0, False, "AES-128-ECB encrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
     "c2_keyed": (65536, 16, 1, False, "C2 with a key id per page (8 AES-128 keys, uniform), HBM, out-of-place"),
     "c3_keyed": (262144, 32, 0, False, "C3 with a key id per page (8 AES-256 keys, uniform), HBM, out-of-place"),
+    "c2_inplace": (65536, 16, 1, True, "C2 in place (AES-128-CBC decrypt, 65,536 x 4 KiB pages), HBM"),
+    "ecb_dec_inplace": (65536, 16, 1, True, "AES-128-ECB decrypt in place, 65,536 x 4 KiB pages, HBM"),
 }
 KEYED = ("c2_keyed", "c3_keyed")
-MODE_OF = {"ecb_dec": 1, "ecb_enc": 1}
+MODE_OF = {"ecb_dec": 1, "ecb_enc": 1, "ecb_dec_inplace": 1}
 SM_COUNT = 148
 LDS_LANES_PER_CLK = 32      # lane-lookups/clk/SM (B300_MICROARCH.md "smem crossbar 128/N B/cyc/SM"; tools/pipes.cu measures it)
 
