@@ -1,32 +1,47 @@
 #!/usr/bin/env python
-"""bench.py -- AES-CBC page-crypto throughput on B200 (BASELINE.json metric).
+"""bench.py -- AES-CBC page-crypto throughput on B200 (BASELINE.json metric:
+"AES-CBC page crypto GB/s (HBM & pinned-host) at 1/2/4/8 B200; % of roofline").
 
-Default workload (N=1, the configuration BASELINE.json's metric is quoted on,
-configs[1]): "eCryptfs-shaped read": AES-128-CBC DECRYPT of a 256 MiB batch
-of 65,536 independent 4 KiB pages with per-page IVs, HBM-resident.  One
-step = one pass of the whole hot path over one batch: kg_submit_pages
-(validate, snapshot key, enqueue) -> the decrypt kernel -> completion ticket
-(kg_wait).  Keys are expanded once (kg_set_key), outside the timed region
-("key expansion once per key", BASELINE.json:5).
+Headline (`value`, the configuration BASELINE.json's metric is quoted on,
+configs[1] = C2): "eCryptfs-shaped read": AES-128-CBC DECRYPT of a 256 MiB
+batch of 65,536 independent 4 KiB pages with per-page IVs, HBM-resident,
+per GPU (weak scaling).  One step = one pass of the whole hot path over one
+batch: kg_submit_pages (validate, snapshot key, enqueue) -> the decrypt
+kernel -> completion ticket (kg_wait).  Keys are expanded once (kg_set_key),
+outside the timed region ("key expansion once per key", BASELINE.json:5).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c5]
-  torchrun ... bench.py --gpus N     (one rank per GPU, NCCL; weak scaling:
-                                      every rank decrypts its own 256 MiB)
-  python bench.py --impl reference   (the oracle on the host cores: a
-                                      bounded sample of the same workload)
+The same JSON line carries, under "configs", every other BASELINE config
+timed the same way with its own roofline, traffic, check, e2e and clocks:
+  c3       AES-256-CBC encrypt, 1 GiB per GPU (configs[2]; the north star's
+           "1 GiB batches")
+  c4_1gib  AES-128-CBC decrypt, 1 GiB per GPU (the top of the configs[3] sweep)
+  c5       AES-128-CBC decrypt of 64 GiB in place, page-range sharded over the
+           ranks (configs[4]; strong scaling: the 1/2/4/8 curve)
+and "c4_sweep" (rank 0, one GPU): caller-observed latency from 1 page to
+1 GiB, HBM and pinned host, beside the oracle (1 and T threads) and
+single-core OpenSSL (context), with the GPU/CPU crossovers.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4_1gib|c5|...]
+      N > 1 without WORLD_SIZE in the environment: re-launches itself under
+      torch.distributed.run with N ranks (one per GPU, NCCL).
+  torchrun --nproc-per-node N ... bench.py --gpus N    (the same, launched by the caller)
+  python bench.py --impl reference   (the oracle on the host cores: a bounded
+                                      sample of the same workload)
 
 Prints ONE JSON line on rank 0.  `value` = payload GB/s (10^9 page bytes per
 second, IVs excluded) over all ranks, device-timed with CUDA events on the
 launching stream, max over ranks.  `e2e` = the same metric through the C ABI
-with pinned HOST buffers (H2D + kernel + D2H inside the timed region, i.e.
-the pinned-host-resident figure of the metric).  See DESIGN.md §Measurement.
+with NUMA-local pinned HOST buffers (H2D + kernel + D2H inside the timed
+region: the pinned-host-resident figure of the metric).  DESIGN.md §9.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -41,21 +56,28 @@ import synth  # noqa: E402
 
 METRIC = "AES-CBC page crypto GB/s (HBM & pinned-host) at 1/2/4/8 B200; % of roofline"
 PB = 4096
+M_PERIOD = 65537        # C5: page p holds page p mod M of a seeded M-page set
+
+# name: (n_pages per rank (weak) or in total (strong), key_bytes, dir, mode, in_place, scaling, description)
 WORKLOADS = {
-    # name: (n_pages per rank, key_bytes, dir, in_place, description)
-    "c2": (65536, 16, 1, False, "C2 eCryptfs-shaped read: AES-128-CBC decrypt, 65,536 x 4 KiB pages (256 MiB) per GPU, HBM-resident, out-of-place"),
-    "c3": (262144, 32, 0, False, "C3 eCryptfs-shaped write: AES-256-CBC encrypt (page-parallel chains), 262,144 x 4 KiB pages (1 GiB) per GPU, HBM-resident"),
-    "c5": (16777216, 16, 1, True, "C5: AES-128-CBC decrypt of 64 GiB (16,777,216 x 4 KiB pages) page-range sharded over the ranks, HBM-resident, in place"),
-    # not BASELINE configs: the paper's own ECB mode (row f1) and mixed-key batches
-    "ecb_dec": (65536, 16, 1, False, "AES-128-ECB decrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
-    "ecb_enc": (65536, 16, 0, False, "AES-128-ECB encrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
-    "c2_keyed": (65536, 16, 1, False, "C2 with a key id per page (8 AES-128 keys, uniform), HBM, out-of-place"),
-    "c3_keyed": (262144, 32, 0, False, "C3 with a key id per page (8 AES-256 keys, uniform), HBM, out-of-place"),
-    "c2_inplace": (65536, 16, 1, True, "C2 in place (AES-128-CBC decrypt, 65,536 x 4 KiB pages), HBM"),
-    "ecb_dec_inplace": (65536, 16, 1, True, "AES-128-ECB decrypt in place, 65,536 x 4 KiB pages, HBM"),
+    "c2": (65536, 16, 1, 0, False, "weak",
+           "C2 eCryptfs-shaped read: AES-128-CBC decrypt, 65,536 x 4 KiB pages (256 MiB) per GPU, HBM-resident, out-of-place"),
+    "c3": (262144, 32, 0, 0, False, "weak",
+           "C3 eCryptfs-shaped write: AES-256-CBC encrypt (page-parallel chains), 262,144 x 4 KiB pages (1 GiB) per GPU, HBM-resident"),
+    "c4_1gib": (262144, 16, 1, 0, False, "weak",
+                "C4 at 1 GiB (top of the batch-size sweep): AES-128-CBC decrypt, 262,144 x 4 KiB pages per GPU, HBM-resident"),
+    "c5": (16777216, 16, 1, 0, True, "strong",
+           "C5: AES-128-CBC decrypt of 64 GiB (16,777,216 x 4 KiB pages) page-range sharded over the ranks, HBM-resident, in place"),
+    # not BASELINE configs: the paper's own ECB mode (row f1), mixed-key batches, in place
+    "ecb_dec": (65536, 16, 1, 1, False, "weak", "AES-128-ECB decrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
+    "ecb_enc": (65536, 16, 0, 1, False, "weak", "AES-128-ECB encrypt (the paper's mode, PAPER.md:448-450), 65,536 x 4 KiB pages, HBM"),
+    "c2_keyed": (65536, 16, 1, 0, False, "weak", "C2 with a key id per page (8 AES-128 keys, uniform), HBM, out-of-place"),
+    "c3_keyed": (262144, 32, 0, 0, False, "weak", "C3 with a key id per page (8 AES-256 keys, uniform), HBM, out-of-place"),
+    "c2_inplace": (65536, 16, 1, 0, True, "weak", "C2 in place (AES-128-CBC decrypt, 65,536 x 4 KiB pages), HBM"),
+    "ecb_dec_inplace": (65536, 16, 1, 1, True, "weak", "AES-128-ECB decrypt in place, 65,536 x 4 KiB pages, HBM"),
 }
 KEYED = ("c2_keyed", "c3_keyed")
-MODE_OF = {"ecb_dec": 1, "ecb_enc": 1, "ecb_dec_inplace": 1}
+DEFAULT_EXTRA = ("c3", "c4_1gib", "c5")
 SM_COUNT = 148
 LDS_LANES_PER_CLK = 32      # lane-lookups/clk/SM (B300_MICROARCH.md "smem crossbar 128/N B/cyc/SM"; tools/pipes.cu measures it)
 
@@ -66,10 +88,51 @@ def nr_of(key_bytes):
 
 def compute_peak_gbs(key_bytes, sm_mhz, sms=SM_COUNT):
     """T-table compute ceiling in payload GB/s: 16*Nr lane-lookups per 16-byte
-    block at LDS_LANES_PER_CLK per SM per clock (DESIGN.md §Roofline)."""
+    block at LDS_LANES_PER_CLK per SM per clock (DESIGN.md §6)."""
     return sms * sm_mhz * 1e6 * LDS_LANES_PER_CLK * 16.0 / (16.0 * nr_of(key_bytes)) / 1e9
 
 
+# ----------------------------------------------------------------------------- multi-rank plan (tested on CPU)
+def plan(workload, rank, world):
+    """This rank's share of a workload: (first_page, n_pages, scaling).
+    Weak scaling: every rank its own full batch (pages [rank*n, (rank+1)*n) of
+    the seeded stream).  Strong scaling (C5): contiguous page range
+    [floor(rN/W), floor((r+1)N/W)) of the one job."""
+    n_total, _, _, _, _, scaling, _ = WORKLOADS[workload]
+    if scaling == "strong":
+        lo, hi = synth.shard(n_total, rank, world)
+        return lo, hi - lo, scaling
+    return rank * n_total, n_total, scaling
+
+
+def job_bytes(workload, world, steps):
+    """Payload bytes the whole job (all ranks) processes in `steps` steps."""
+    n_total, _, _, _, _, scaling, _ = WORKLOADS[workload]
+    per_step = n_total * PB * (world if scaling == "weak" else 1)
+    return per_step * steps
+
+
+def reduce_max(dist, values, device):
+    """MAX over ranks of a list of floats (the timing reduction)."""
+    if dist is None:
+        return [float(v) for v in values]
+    import torch
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def reduce_sum(dist, values, device):
+    """SUM over ranks of a list of floats (check counters)."""
+    if dist is None:
+        return [float(v) for v in values]
+    import torch
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.tolist()]
+
+
+# ----------------------------------------------------------------------------- peaks, traffic, clocks
 def load_peaks():
     """Driver-written measured peaks; tolerant of the key names (the HBM copy
     bandwidth and the max SM clock are all bench.py reads), else the
@@ -112,7 +175,8 @@ def load_traffic(workload):
 
 
 class ClockSampler:
-    """pynvml sampling of SM clock + throttle reasons during the timed region."""
+    """pynvml sampling of SM clock + throttle reasons during a timed region
+    (every `period` s, plus one sample at entry and one at exit)."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -120,7 +184,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index, period=0.005):
+    def __init__(self, pci_bus_id=None, index=0, period=0.001):
         self.ok = False
         self.samples, self.reasons = [], set()
         self.period = period
@@ -128,7 +192,15 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.h = None
+            if pci_bus_id:
+                try:
+                    self.h = pynvml.nvmlDeviceGetHandleByPciBusId(pci_bus_id.encode() if isinstance(pci_bus_id, str)
+                                                                   else pci_bus_id)
+                except Exception:  # noqa: BLE001
+                    self.h = None
+            if self.h is None:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception:  # noqa: BLE001
@@ -136,20 +208,24 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _one(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
+            self._one()
             time.sleep(self.period)
 
     def __enter__(self):
         if self.ok:
+            self._one()
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
@@ -158,24 +234,41 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join()
+            self._one()
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_min_mhz": min(self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def duplex_link_gbs(torch, h_a, h_b, nbytes=128 << 20, reps=5):
-    """Measured concurrent H2D + D2H pinned copy bandwidth per direction (the
-    pinned-host path's roofline: every payload byte crosses the link both ways)."""
+def merge_clocks(parts):
+    """Clock summaries of several ranks / regions -> one (min of medians, union of reasons)."""
+    parts = [p for p in parts if p and p.get("samples")]
+    if not parts:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+    return {"sm_mhz": min(p["sm_mhz"] for p in parts), "sm_min_mhz": min(p.get("sm_min_mhz", p["sm_mhz"]) for p in parts),
+            "sm_max_mhz": max((p["sm_max_mhz"] or 0) for p in parts) or None,
+            "reasons": sorted(set().union(*[set(p["reasons"]) for p in parts])),
+            "samples": sum(p["samples"] for p in parts), "ranks_or_regions": len(parts)}
+
+
+def duplex_link(torch, dist, red_dev, h_a, h_b, nbytes=128 << 20, reps=5):
+    """Pinned-host link bound: concurrent H2D + D2H copies (every payload byte
+    crosses the link both ways), all ranks copying at once (a barrier before
+    each rep).  Returns (per-rank GB/s per direction, aggregate GB/s per
+    direction over all ranks = W * bytes / max-rank time)."""
     nbytes = min(nbytes, h_a.numel(), h_b.numel())
     d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-    best = None
+    best, best_max = None, None
+    world = dist.get_world_size() if dist else 1
     for _ in range(reps):
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         s1.wait_event(e0)
@@ -189,15 +282,11 @@ def duplex_link_gbs(torch, h_a, h_b, nbytes=128 << 20, reps=5):
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 1e3
+        tmax = reduce_max(dist, [t], red_dev)[0]
         best = t if best is None else min(best, t)
-    return nbytes / best / 1e9
-
-
-def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+        best_max = tmax if best_max is None else min(best_max, tmax)
+    del d_a, d_b
+    return nbytes / best / 1e9, world * nbytes / best_max / 1e9
 
 
 # ----------------------------------------------------------------------------- oracle (reference arm / cpu_baseline)
@@ -221,11 +310,42 @@ def oracle_rate(n_pages_cap, key_bytes, direction, target_s, threads):
     return n * PB / dt / 1e9, n, dt
 
 
+def openssl_rate(key_bytes, direction, target_s=2.0):
+    """Context, NOT the oracle: single-core OpenSSL (AES-NI) CBC through the
+    `cryptography` package, one cipher context per 4 KiB page (as a
+    filesystem would call it), on a bounded sample.  The paper's comparator
+    was an SSE-optimised in-kernel AES."""
+    try:
+        from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": repr(e)}
+    key = synth.make_key(key_bytes)
+    n = 4096
+    data = synth.make_pages(n, PB).tobytes()
+    ivs = synth.make_ivs(n).tobytes()
+
+    def one_pass():
+        for p in range(n):
+            c = Cipher(algorithms.AES(key), modes.CBC(ivs[16 * p:16 * p + 16]))
+            x = c.decryptor() if direction else c.encryptor()
+            x.update(data[p * PB:(p + 1) * PB])
+
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < target_s or reps == 0:
+        one_pass()
+        reps += 1
+    dt = time.perf_counter() - t0
+    return {"value": reps * n * PB / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "openssl_aesni_context (not the oracle)",
+            "sample": f"{reps} x {n} seeded 4 KiB pages, one cipher context per page, {dt:.1f} s"}
+
+
 def run_reference(args):
-    world, rank, _ = dist_env()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    n_pages, key_bytes, direction, _, desc = WORKLOADS[args.workload]
+    n_pages, key_bytes, direction, mode, _, scaling, desc = WORKLOADS[args.workload]
     threads = len(os.sched_getaffinity(0))
     per_step = args.ref_step_seconds or max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
     import oracle
@@ -235,11 +355,11 @@ def run_reference(args):
     data = synth.make_pages(n, PB)
     ivs = synth.make_ivs(n)
     for _ in range(args.warmup):
-        oracle.pages(direction, 0, key, data, n, PB, ivs, threads=threads)
+        oracle.pages(direction, mode, key, data, n, PB, ivs, threads=threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.pages(direction, 0, key, data, n, PB, ivs, threads=threads)
+        oracle.pages(direction, mode, key, data, n, PB, ivs, threads=threads)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     gbs = n * PB * args.steps / total / 1e9
@@ -247,9 +367,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": desc, "n_pages": n_pages, "page_bytes": PB, "key_bits": 8 * key_bytes,
-                   "dir": "decrypt" if direction else "encrypt", "sampled_pages_per_step": n},
+                   "dir": "decrypt" if direction else "encrypt", "sampled_pages_per_step": n,
+                   "world_ranks_present": world},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -258,65 +379,96 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
-def run_ours(args):
-    import torch
+class Ctx:
+    """Per-process state of our arm (rank, device, process group)."""
 
-    import paper_1305_3345_b200 as kg
+    def __init__(self, args):
+        import torch
+        self.torch = torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # one process per GPU; KG_BENCH_SHARE_GPU=1 (testing the N>1 code path
+        # on a one-GPU box) maps ranks onto the available devices and uses gloo
+        self.share = os.environ.get("KG_BENCH_SHARE_GPU") == "1"
+        self.dev = self.local % torch.cuda.device_count() if self.share else self.local
+        torch.cuda.set_device(self.dev)
+        self.dist = None
+        self.red_dev = "cpu"
+        self.comm = {"backend": None, "world": 1}
+        if self.world > 1:
+            import torch.distributed as dist
+            if self.share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.dev))
+                self.red_dev = "cuda"
+            self.dist = dist
+            one = torch.ones(1, dtype=torch.float64, device=self.red_dev)
+            dist.all_reduce(one)
+            self.comm = {"backend": dist.get_backend(), "world": dist.get_world_size(),
+                         "allreduce_sum_of_ones": int(one.item())}
+        try:
+            self.pci = torch.cuda.get_device_properties(self.dev).pci_bus_id
+        except Exception:  # noqa: BLE001
+            self.pci = None
 
-    world, rank, local = dist_env()
-    if not torch.cuda.is_available():
-        print(json.dumps({"error": "no CUDA device"}))
-        return 1
-    # one process per GPU; KG_BENCH_SHARE_GPU=1 (testing the N>1 code path on a
-    # one-GPU box) maps ranks onto the available devices and uses gloo
-    share = os.environ.get("KG_BENCH_SHARE_GPU") == "1"
-    dev = local % torch.cuda.device_count() if share else local
-    torch.cuda.set_device(dev)
-    dist = None
-    red_dev = "cuda"
-    if world > 1:
-        import torch.distributed as dist
-        if share:
-            dist.init_process_group("gloo")
-            red_dev = "cpu"
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    kg.init(dev)
-    n_total, key_bytes, direction, in_place, desc = WORKLOADS[args.workload]
-    if args.workload == "c5":
-        lo, hi = synth.shard(n_total, rank, world)   # strong scaling: 64 GiB split by page range
-        scaling = "strong"
-    else:
-        lo, hi = 0, n_total                           # weak scaling: every rank its own batch
-        scaling = "weak"
-    n = hi - lo
-    key = synth.make_key(key_bytes)
-    kg.set_key(0, key)
-    mode = MODE_OF.get(args.workload, kg.MODE_CBC)
-    keyed = args.workload in KEYED
-    if keyed:
-        for i in range(8):
-            kg.set_key(i, synth.make_key(key_bytes, seed=synth.KEY_SEED + 100 + i))
-    stream = torch.cuda.current_stream()
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.dist:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
 
-    # inputs: seeded pages (C2/C3: the full batch; C5: periodic M-page pattern)
-    M = 65537
-    if args.workload == "c5":
+    def gather(self, obj):
+        if not self.dist:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+
+def make_inputs(ctx, workload, first, n):
+    """Seeded device inputs of this rank (untimed).  C5: the periodic M-page pattern."""
+    torch = ctx.torch
+    if workload == "c5":
+        M = M_PERIOD
         pat = torch.from_numpy(synth.make_pages(M, PB)).cuda().view(M, PB)
         ivp = torch.from_numpy(synth.make_ivs(M)).cuda().view(M, 16)
         x = torch.empty((n, PB), dtype=torch.uint8, device="cuda")
         ivs = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
-        for s in range(0, n, M):
-            e = min(n, s + M)
-            idx = (torch.arange(s, e, device="cuda") + lo) % M
-            x[s:e] = pat[idx]
-            ivs[s:e] = ivp[idx]
-        del pat, ivp
-        x = x.view(-1)
-        ivs = ivs.view(-1)
-    else:
-        x = torch.from_numpy(synth.make_pages(n, PB, first_page=lo)).cuda()
-        ivs = torch.from_numpy(synth.make_ivs(n, first_page=lo)).cuda()
+        fill_periodic(torch, x, ivs, pat, ivp, first)
+        return x.view(-1), ivs.view(-1), (pat, ivp)
+    x = torch.from_numpy(synth.make_pages(n, PB, first_page=first)).cuda()
+    ivs = torch.from_numpy(synth.make_ivs(n, first_page=first)).cuda()
+    return x, ivs, None
+
+
+def fill_periodic(torch, x, ivs, pat, ivp, first):
+    """x[p] = pat[(first + p) mod M] (device copies)."""
+    n, M = x.shape[0], pat.shape[0]
+    p = 0
+    while p < n:
+        src = (first + p) % M
+        cnt = min(n - p, M - src)
+        x[p:p + cnt].copy_(pat[src:src + cnt])
+        ivs[p:p + cnt].copy_(ivp[src:src + cnt])
+        p += cnt
+
+
+def run_config(ctx, args, workload, steps, warmup, want_e2e=True):
+    """Time one workload on every rank; returns the rank-0 summary dict (None elsewhere)."""
+    import paper_1305_3345_b200 as kg
+    torch = ctx.torch
+    n_total, key_bytes, direction, mode, in_place, scaling, desc = WORKLOADS[workload]
+    first, n, _ = plan(workload, ctx.rank, ctx.world)
+    keyed = workload in KEYED
+    key = synth.make_key(key_bytes)
+    kg.set_key(0, key)
+    if keyed:
+        for i in range(8):
+            kg.set_key(i, synth.make_key(key_bytes, seed=synth.KEY_SEED + 100 + i))
+    stream = torch.cuda.current_stream()
+    x, ivs, pattern = make_inputs(ctx, workload, first, n)
     out = x if in_place else torch.empty_like(x)
     key_ids = None
     if keyed:
@@ -324,211 +476,394 @@ def run_ours(args):
                                    .astype(np.int16)).cuda()
     torch.cuda.synchronize()
 
-    def step():
+    def step(dst=None, src=None, d=direction):
+        s_in = x if src is None else src
+        s_out = out if dst is None else dst
         if keyed:
-            return kg.submit_pages_keyed(direction, mode, x, out, n, PB, ivs, key_ids, key_bytes, stream)
-        return kg.submit_pages(direction, mode, x, out, n, PB, ivs if mode == kg.MODE_CBC else None, 0, stream)
+            return kg.submit_pages_keyed(d, mode, s_in, s_out, n, PB, ivs if mode == 0 else None, key_ids, key_bytes,
+                                         stream)
+        return kg.submit_pages(d, mode, s_in, s_out, n, PB, ivs if mode == 0 else None, 0, stream)
 
-    # warm-up (also loads the module lazily)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         kg.wait(step())
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
+    ctx.barrier()
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = kg.launch_count()
-    with ClockSampler(dev) as clk:
+    with ClockSampler(ctx.pci, ctx.dev) as clk:
         t_wall0 = time.perf_counter()
-        tickets = []
-        for i in range(args.steps):
-            if args.step_events or i == 0:
-                starts[i].record(stream)
-            tickets.append(step())
-            if args.step_events or i == args.steps - 1:
-                ends[i].record(stream)
+        ev0.record(stream)
+        tickets = [step() for _ in range(steps)]
+        ev1.record(stream)
         for t in tickets:
             kg.wait(t)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     launches = kg.launch_count() - l0
-    elapsed = starts[0].elapsed_time(ends[-1]) / 1e3                   # s, device-timed
-    if args.step_events:
-        per_launch = [s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)]
-        avg_launch = sum(per_launch) / max(launches, len(per_launch))
-    else:
-        # launches back to back on one stream; a step is one launch, or several
-        # page windows when the input exceeds one texture (C5)
-        avg_launch = elapsed / max(launches, args.steps)
-    if dist:
-        t = torch.tensor([elapsed, avg_launch], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed, avg_launch = float(t[0]), float(t[1])
-    bytes_step = n * PB
-    total_bytes = bytes_step * args.steps * (world if scaling == "weak" else 1)
-    if scaling == "strong":
-        total_bytes = n_total * PB * args.steps
-    value = total_bytes / elapsed / 1e9
-    clocks = clk.summary()
+    elapsed = ev0.elapsed_time(ev1) / 1e3                 # s, device-timed on the launching stream
+    avg_launch = elapsed / max(launches, steps)           # launches back to back on one stream
+    elapsed_max, avg_launch_max = reduce_max(ctx.dist, [elapsed, avg_launch], ctx.red_dev)
+    value = job_bytes(workload, ctx.world, steps) / elapsed_max / 1e9
+    clocks = merge_clocks(ctx.gather(clk.summary()))
+    launches_all = int(reduce_sum(ctx.dist, [launches], ctx.red_dev)[0])
 
-    # correctness check outside the timed region (every rank, SUM over ranks):
-    # one more step, then S sampled output pages go back through the inverse
-    # operation on the GPU and must reproduce the step's input pages.
+    # correctness check outside the timed region (every rank, SUM over ranks)
     check = None
     if not args.no_check:
-        S = min(n, 1024)
-        gen = torch.Generator().manual_seed(1305 + rank)
-        idx = torch.randperm(n, generator=gen)[:S].sort().values.cuda()
-        xv = x.view(n, PB)
-        before = xv[idx].clone()
-        kg.wait(step())
-        torch.cuda.synchronize()
-        after = out.view(n, PB)[idx].contiguous()
-        iv_s = ivs.view(n, 16)[idx].contiguous().view(-1) if mode == kg.MODE_CBC else None
-        back = torch.empty_like(after)
-        inv = 1 - direction
-        if keyed:
-            kid_s = key_ids[idx].contiguous()
-            kg.wait(kg.submit_pages_keyed(inv, mode, after.view(-1), back.view(-1), S, PB, iv_s, kid_s, key_bytes, stream))
+        if workload == "c5":
+            # one step on freshly filled pages; EVERY byte is compared on the
+            # device with one launch over the M-page pattern (pages are
+            # independent; tests/test_fullsize_gpu.py anchors that run to the oracle)
+            pat, ivp = pattern
+            fill_periodic(torch, x.view(n, PB), ivs.view(n, 16), pat, ivp, first)
+            kg.wait(step())
+            ref = torch.empty_like(pat)
+            kg.wait(kg.submit_pages(direction, mode, pat, ref, M_PERIOD, PB, ivp, 0, stream))
+            bad = 0
+            xv = x.view(n, PB)
+            for s in range(0, n, M_PERIOD):
+                e = min(n, s + M_PERIOD)
+                src = (first + s) % M_PERIOD
+                cnt = e - s
+                if src + cnt <= M_PERIOD:
+                    exp = ref[src:src + cnt]
+                else:
+                    exp = torch.cat([ref[src:], ref[:cnt - (M_PERIOD - src)]])
+                bad += int((xv[s:e] != exp).any(dim=1).sum())
+            del ref
+            tot = reduce_sum(ctx.dist, [bad, n], ctx.red_dev)
+            check = {"pages": int(tot[1]), "mismatched_pages": int(tot[0]),
+                     "method": "every byte of one fresh step vs one launch over the M=65,537-page pattern "
+                               "(periodic input; oracle anchoring of that run: tests/test_fullsize_gpu.py)"}
         else:
-            kg.wait(kg.submit_pages(inv, mode, after.view(-1), back.view(-1), S, PB, iv_s, 0, stream))
-        torch.cuda.synchronize()
-        bad = torch.tensor([float((back != before).any(dim=1).sum()), float(S)], dtype=torch.float64, device=red_dev
-                           if dist else "cpu")
-        if dist:
-            dist.all_reduce(bad, op=dist.ReduceOp.SUM)
-        check = {"sampled_pages": int(bad[1]), "mismatched_pages": int(bad[0]),
-                 "method": "one extra step; sampled output pages through the inverse operation on the GPU "
-                           "must give back the step's input pages (parity vs the oracle: tests/)"}
+            # one more step, then EVERY output page goes back through the
+            # inverse operation on the GPU and must reproduce the step's input
+            before = x.clone() if in_place else x
+            kg.wait(step())
+            back = torch.empty_like(x)
+            inv = 1 - direction
+            if keyed:
+                kg.wait(kg.submit_pages_keyed(inv, mode, out, back, n, PB, ivs if mode == 0 else None, key_ids,
+                                              key_bytes, stream))
+            else:
+                kg.wait(kg.submit_pages(inv, mode, out, back, n, PB, ivs if mode == 0 else None, 0, stream))
+            torch.cuda.synchronize()
+            bad = int((back.view(n, PB) != before.view(n, PB)).any(dim=1).sum())
+            del back, before
+            tot = reduce_sum(ctx.dist, [bad, n], ctx.red_dev)
+            check = {"pages": int(tot[1]), "mismatched_pages": int(tot[0]),
+                     "method": "one extra step; every output page through the inverse operation on the GPU must "
+                               "give back the step's input page (byte-exact parity vs the oracle: tests/)"}
+    del pattern
 
-    # secondary: e2e through the C ABI with pinned HOST buffers (H2D + compute + D2H timed)
+    # e2e through the C ABI with NUMA-local pinned HOST buffers (H2D + compute + D2H timed)
     e2e = None
-    if args.workload in ("c2", "c3", "c5") and not args.no_e2e:
-        big = args.workload == "c5"            # 64 GiB: NUMA-local pinned shard, in place
-        e_steps = max(1, min(args.steps, 2 if big else args.e2e_steps))
-        if big:
-            hx = kg.alloc_pinned(n * PB)
-            hx.copy_(x)
-            hiv = kg.alloc_pinned(16 * n)
-            hiv.copy_(ivs)
-            hout = hx
-            residency = "pinned host shard (kg_alloc_pinned: cudaHostAlloc from GPU-local CPUs), in place"
-        else:
-            hx = torch.empty(n * PB, dtype=torch.uint8).pin_memory()
-            hx.copy_(x.cpu())
-            hiv = ivs.cpu().pin_memory()
-            hout = hx if in_place else torch.empty_like(hx).pin_memory()
-            residency = "pinned host (cudaHostAlloc via torch pin_memory)"
+    if want_e2e and not args.no_e2e and not keyed:
+        big = workload == "c5"
+        e_steps = max(1, min(steps, 2 if big else args.e2e_steps))
+        hx = kg.alloc_pinned(n * PB)
+        hx.copy_(x)
+        hiv = kg.alloc_pinned(16 * n)
+        hiv.copy_(ivs)
+        hout = hx if in_place else kg.alloc_pinned(n * PB)
+        del x, out, ivs
+        torch.cuda.empty_cache()
+        residency = ("pinned host (kg_alloc_pinned: cudaHostAlloc from a thread on the GPU-local CPUs)"
+                     + (", in place" if in_place else ""))
         for _ in range(1 if big else 2):
-            kg.wait(kg.submit_pages(direction, kg.MODE_CBC, hx, hout, n, PB, hiv, 0, stream))
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
+            kg.wait(kg.submit_pages(direction, mode, hx, hout, n, PB, hiv if mode == 0 else None, 0, stream))
+        ctx.barrier()
         step_ms = []
         t0 = time.perf_counter()
         for _ in range(e_steps):
             ts = time.perf_counter()
-            kg.wait(kg.submit_pages(direction, kg.MODE_CBC, hx, hout, n, PB, hiv, 0, stream))
+            kg.wait(kg.submit_pages(direction, mode, hx, hout, n, PB, hiv if mode == 0 else None, 0, stream))
             step_ms.append((time.perf_counter() - ts) * 1e3)
         te = time.perf_counter() - t0
-        if dist:
-            tt = torch.tensor([te], dtype=torch.float64, device=red_dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt[0])
-        total_e2e = (n_total * PB if scaling == "strong" else bytes_step * world) * e_steps
-        e2e = {"value": total_e2e / te / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": bytes_step + 16 * n, "d2h_bytes_per_step": bytes_step,
-               "steps": e_steps, "residency": residency,
+        te_max = reduce_max(ctx.dist, [te], ctx.red_dev)[0]
+        e2e = {"value": job_bytes(workload, ctx.world, e_steps) / te_max / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": n * PB + (16 * n if mode == 0 else 0), "d2h_bytes_per_step": n * PB,
+               "steps": e_steps, "residency": residency, "timing": "wall clock around submit + kg_wait, max over ranks",
                "step_ms_min_median_max": [round(min(step_ms), 3), round(sorted(step_ms)[len(step_ms) // 2], 3),
                                           round(max(step_ms), 3)]}
-        # host-link roofline for this path: pinned H2D and D2H copy engines at once
-        link = duplex_link_gbs(torch, hx, hout)
-        e2e["link_duplex_gbs_per_direction"] = link
-        e2e["link_frac"] = (e2e["value"] / world) / link if link else None
-        if big:
-            kg.free_pinned(hx)
-            kg.free_pinned(hiv)
+        per_rank, agg = duplex_link(torch, ctx.dist, ctx.red_dev, hx, hout)
+        e2e["link_duplex_gbs_per_direction"] = per_rank
+        e2e["link_duplex_aggregate_gbs_per_direction"] = agg
+        e2e["link_frac"] = e2e["value"] / agg if agg else None
+        e2e["link_note"] = ("bound = concurrent pinned H2D + D2H copies measured with all ranks copying at once "
+                            "(aggregate over ranks, per direction)")
+        kg.free_pinned(hx)
+        kg.free_pinned(hiv)
+        if not in_place:
+            kg.free_pinned(hout)
         del hx, hout, hiv
+    else:
+        del x, out, ivs
+    del key_ids
+    torch.cuda.empty_cache()
 
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
-        return 0
-
+    if ctx.rank != 0:
+        return None
     peaks = load_peaks()
     sm_max = float(clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
-    launches_per_step = max(1, launches // args.steps)
-    bytes_launch = bytes_step / launches_per_step
-    achieved = bytes_launch / avg_launch / 1e9
+    launches_per_step = max(1, launches // steps)
+    bytes_launch = n * PB / launches_per_step
+    achieved = bytes_launch / avg_launch_max / 1e9
     peak = compute_peak_gbs(key_bytes, sm_max)
+    chain = direction == 0 and mode == 0
+    kernel = (("kg_keyed_chain" if chain else "kg_keyed_pair") if keyed
+              else "kg_cbc_enc" if chain else "kg_blockpar") + \
+        f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>"
     roof = {
         "bound": "alu", "pipe": "lds (shared-memory T-table lookups: 16*Nr lane-lookups per 16-byte block)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": load_traffic(args.workload),
+        "traffic": load_traffic(workload),
         "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/traffic.json)",
-        "peak_basis": f"{SM_COUNT} SMs x {sm_max:.0f} MHz (sm_max) x {LDS_LANES_PER_CLK} lane-lookups/clk/SM / (16*Nr lookups per 16 B)",
+        "peak_basis": f"{SM_COUNT} SMs x {sm_max:.0f} MHz (sm_max) x {LDS_LANES_PER_CLK} lane-lookups/clk/SM / "
+                      f"(16*Nr lookups per 16 B)",
         "frac_at_measured_clock": (achieved / compute_peak_gbs(key_bytes, clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
         "hbm_payload_peak": peaks["hbm_gbs"] / (2 + 16.0 / PB),
         "hbm_peak_source": ("fallback 6650 GB/s (no MEASURED_PEAKS.json)" if peaks.get("_fallback")
                             else "MEASURED_PEAKS.json"),
         "hbm_frac": achieved / (peaks["hbm_gbs"] / (2 + 16.0 / PB)),
-        "kernel": (("kg_keyed_chain" if (direction == 0 and mode == kg.MODE_CBC) else "kg_keyed_pair") if keyed
-                   else "kg_blockpar" if (direction == 1 or mode == kg.MODE_ECB) else "kg_cbc_enc") + f"<Nr={nr_of(key_bytes)},{'dec' if direction else 'enc'},{'ecb' if mode else 'cbc'}>",
-        "algorithmic_bytes_per_launch": bytes_launch,
-        "launches_per_step": launches_per_step,
+        "kernel": kernel, "algorithmic_bytes_per_launch": bytes_launch, "launches_per_step": launches_per_step,
+        "avg_launch_ms": 1e3 * avg_launch_max,
         "page_loads": "LDG" if os.environ.get("KG_TEXIN") == "0" else "texture pipe (TLD)",
     }
-    line = {
-        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-        "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": desc, "n_pages_per_gpu": n, "page_bytes": PB, "key_bits": 8 * key_bytes,
-                   "dir": "decrypt" if direction else "encrypt", "mode": "ecb" if mode else "cbc", "residency": "hbm",
-                   "l2": f"no flush: each step reads {bytes_step / 2**20:.0f} MiB and writes "
-                         f"{bytes_step / 2**20:.0f} MiB, > 126 MB L2",
-                   "parallelism": f"page-range x{world}" if world > 1 else "1 GPU"},
-        "roofline": roof,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "check": check,
-        "clocks": clocks,
+    return {
+        "workload": desc, "name": workload, "value": value, "unit": "GB/s", "ms_per_step": 1e3 * elapsed_max / steps,
+        "steps": steps, "warmup": warmup, "scaling": scaling, "n_pages_per_gpu": n, "n_pages_total":
+            n_total * (ctx.world if scaling == "weak" else 1), "key_bits": 8 * key_bytes,
+        "dir": "decrypt" if direction else "encrypt", "mode": "ecb" if mode else "cbc", "in_place": in_place,
+        "roofline": roof, "e2e": e2e, "check": check, "clocks": clocks, "gpu_launches": launches_all,
         "wall_s_timed": t_wall,
+        "l2": (f"no flush: each step reads {n * PB / 2**20:.0f} MiB" +
+               ("" if in_place else f" and writes {n * PB / 2**20:.0f} MiB") + " per GPU, > 126 MB L2"),
     }
-    if world == 1 and not args.no_cpu_baseline:
+
+
+def c4_sweep(ctx, args):
+    """configs[3] on rank 0 (one GPU): caller-observed latency of ONE request
+    (submit -> kg_wait returns) from 1 page to 1 GiB, HBM and pinned host
+    (the library's default host path), beside the oracle and single-core
+    OpenSSL at the same size; crossover = smallest size from which the GPU's
+    p50 stays at or below the CPU's (a tie counts for the GPU)."""
+    import oracle
+    import paper_1305_3345_b200 as kg
+    torch = ctx.torch
+    kmax = args.sweep_kmax
+    nmax = 1 << kmax
+    key = synth.make_key(16)
+    kg.set_key(0, key)
+    threads = len(os.sched_getaffinity(0))
+    data = synth.make_pages(nmax, PB)
+    ivs_np = synth.make_ivs(nmax)
+    dx = torch.from_numpy(data).cuda()
+    div = torch.from_numpy(ivs_np).cuda()
+    dout = torch.empty_like(dx)
+    hx = kg.alloc_pinned(nmax * PB)
+    hx.copy_(torch.from_numpy(data))
+    hout = kg.alloc_pinned(nmax * PB)
+    hiv = kg.alloc_pinned(16 * nmax)
+    hiv.copy_(torch.from_numpy(ivs_np))
+    s = torch.cuda.current_stream()
+    try:
+        from cryptography.hazmat.primitives.ciphers import Cipher, algorithms, modes
+    except Exception:  # noqa: BLE001
+        Cipher = None
+
+    def lat(fn, reps):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return 1e6 * statistics.median(ts)
+
+    rows = []
+    for k in range(kmax + 1):
+        n = 1 << k
+        reps = 50 if n * PB < (1 << 20) else (20 if n * PB < (64 << 20) else 5)
+        row = {"pages": n}
+        for name, (a, b, c) in (("hbm", (dx, dout, div)), ("pinned", (hx, hout, hiv))):
+            def f():
+                kg.wait(kg.submit_pages(1, 0, a, b, n, PB, c, 0, s))
+            for _ in range(3):
+                f()
+            row[f"{name}_us"] = round(lat(f, reps), 2)
+        if n <= args.sweep_nsk_pages:
+            kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+
+            def g():
+                kg.wait(kg.submit_pages(1, 0, dx, dout, n, PB, div, 0, s))
+            for _ in range(3):
+                g()
+            row["nsk_hbm_us"] = round(lat(g, reps), 2)
+            kg.nsk_stop()
+        c_np = data[: n * PB]
+        iv_np = ivs_np[: 16 * n]
+        if n <= 64:
+            row["oracle_1t_us"] = round(lat(lambda: oracle.pages(1, 0, key, c_np, n, PB, iv_np, threads=1),
+                                            5 if n < 16 else 2), 1)
+        if n <= 1024:
+            row["oracle_T_us"] = round(lat(lambda: oracle.pages(1, 0, key, c_np, n, PB, iv_np, threads=threads),
+                                           5 if n < 64 else 2), 1)
+        if Cipher is not None and n <= 4096:
+            cb, ivb = c_np.tobytes(), iv_np.tobytes()
+
+            def ossl():
+                for p in range(n):
+                    Cipher(algorithms.AES(key), modes.CBC(ivb[16 * p:16 * p + 16])).decryptor().update(
+                        cb[p * PB:(p + 1) * PB])
+            row["openssl_1core_us"] = round(lat(ossl, 5 if n < 256 else 2), 1)
+        rows.append(row)
+    kg.free_pinned(hx)
+    kg.free_pinned(hout)
+    kg.free_pinned(hiv)
+    del dx, dout, div
+    torch.cuda.empty_cache()
+
+    def crossover(gk, ck):
+        pts = [r for r in rows if gk in r and ck in r]
+        for r in pts:
+            if all(q[gk] <= q[ck] for q in pts if q["pages"] >= r["pages"]):
+                return {"bytes": r["pages"] * PB, "measured_pages": [pts[0]["pages"], pts[-1]["pages"]]}
+        return {"bytes": None, "measured_pages": [pts[0]["pages"], pts[-1]["pages"]] if pts else None}
+
+    cross = {}
+    for gk in ("hbm_us", "pinned_us", "nsk_hbm_us"):
+        for ck in ("oracle_1t_us", "oracle_T_us", "openssl_1core_us"):
+            cross[f"{gk[:-3]} vs {ck[:-3]}"] = crossover(gk, ck)
+    return {"workload": "C4 request batch-size sweep: AES-128-CBC decrypt, one request of 2^k 4 KiB pages, "
+                        f"k = 0..{kmax}; p50 latency in us (submit -> kg_wait returns)",
+            "oracle_threads": threads, "rows": rows, "crossover": cross,
+            "note": "crossover = smallest size from which the GPU p50 stays <= the CPU's (tie -> GPU); "
+                    "openssl = single-core AES-NI via `cryptography`, context not the oracle; "
+                    "the paper: GPU faster from 8 KB (PAPER.md:460-463)"}
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1305_3345_b200 as kg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a mislabelled "
+                                   "n_gpus", "rank": rank, "world": world}), flush=True)
+        return 2
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device", "rank": rank, "world": world}), flush=True)
+        return 1
+    ctx = Ctx(args)
+    kg.init(ctx.dev)
+
+    head = run_config(ctx, args, args.workload, args.steps, args.warmup)
+    extras = {}
+    if args.workload == "c2" and args.extra != "none":
+        names = DEFAULT_EXTRA if args.extra == "default" else tuple(x for x in args.extra.split(",") if x)
+        for name in names:
+            if name not in WORKLOADS or name == args.workload:
+                continue
+            extras[name] = run_config(ctx, args, name, args.steps, args.warmup)
+    sweep = None
+    if ctx.world == 1 and not args.no_sweep and args.workload == "c2":
+        sweep = c4_sweep(ctx, args)
+
+    if ctx.rank != 0:
+        if ctx.dist:
+            ctx.dist.barrier()
+            ctx.dist.destroy_process_group()
+        return 0
+
+    line = {
+        "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": ctx.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": head["scaling"], "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": head["workload"], "name": args.workload, "n_pages_per_gpu": head["n_pages_per_gpu"],
+                   "page_bytes": PB, "key_bits": head["key_bits"], "dir": head["dir"], "mode": head["mode"],
+                   "residency": "hbm", "in_place": head["in_place"], "l2": head["l2"],
+                   "parallelism": f"page-range x{ctx.world}" if ctx.world > 1 else "1 GPU"},
+        "roofline": head["roofline"],
+        "e2e": head["e2e"],
+        "gpu_launches": head["gpu_launches"],
+        "check": head["check"],
+        "clocks": head["clocks"],
+        "clocks_all_timed_regions": merge_clocks([head["clocks"]] + [c["clocks"] for c in extras.values()]),
+        "comm": ctx.comm,
+        "wall_s_timed": head["wall_s_timed"],
+        "configs": extras,
+    }
+    if sweep:
+        line["c4_sweep"] = sweep
+    if ctx.world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
+        n_total, key_bytes, direction = WORKLOADS[args.workload][:3]
         gbs, npg, dt = oracle_rate(n_total, key_bytes, direction, args.cpu_seconds, threads)
-        line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle",
-                                "sample": f"{npg} seeded 4 KiB pages ({npg * PB / 2**20:.1f} MiB) of the same workload, "
-                                          f"{threads} pthreads, {dt:.1f} s"}
+        g1, n1, d1 = oracle_rate(n_total, key_bytes, direction, args.cpu_seconds / 2, 1)
+        line["cpu_baseline"] = {
+            "value": gbs, "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"{npg} seeded 4 KiB pages ({npg * PB / 2**20:.1f} MiB) of the same workload, "
+                      f"{threads} pthreads, {dt:.1f} s",
+            "one_thread": {"value": g1, "unit": "GB/s", "cores": 1,
+                           "sample": f"{n1} seeded 4 KiB pages ({n1 * PB / 2**20:.1f} MiB), 1 thread, {d1:.1f} s"}}
+        line["context"] = {"openssl_aesni_1core": openssl_rate(key_bytes, direction)}
     print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    if ctx.dist:
+        ctx.dist.barrier()
+        ctx.dist.destroy_process_group()
     return 0
 
 
-def main():
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args, argv):
+    """--gpus N > 1 without a launcher: re-run this script under
+    torch.distributed.run, one rank per GPU (NCCL), rendezvous on 127.0.0.1.
+    NCCL_DEBUG=INFO (INIT subsystem) unless the caller set it, so the log
+    shows the communicator's rank count."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd, env=env)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=30)
-    ap.add_argument("--step-events", action="store_true",
-                    help="record a CUDA event pair around every step (serialises programmatic dependent launch)")
+    ap.add_argument("--extra", default="default",
+                    help="comma list of extra workloads in the same line (with --workload c2); 'none' to skip")
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--sweep-kmax", type=int, default=18)
+    ap.add_argument("--sweep-nsk-pages", type=int, default=256)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-step-seconds", type=float, default=0.0,
                     help="reference arm: oracle seconds per step (default: sized so the run takes ~2.5 min)")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args, argv)
     return run_ours(args)
 
 

@@ -148,7 +148,13 @@ KG_API int kg_wait(int64_t ticket);
 KG_API int kg_poll(int64_t ticket);
 
 /* Drain all outstanding work, free the staging ring, streams, events and
- * tables, forget all keys.  KG_ENOTINIT if not initialised. */
+ * tables, forget all keys.  After an
+ * asynchronous device fault (KG_ECUDA from kg_wait/kg_poll: a sticky CUDA
+ * error) it also resets the device (cudaDeviceReset), so that kg_init can
+ * start again in a fresh context -- every allocation the process made on
+ * that device (the caller's and kg_alloc_pinned buffers included) is gone
+ * then.  KG_ENOTINIT if not
+ * initialised. */
 KG_API int kg_shutdown(void);
 
 /* Static description of a status code; never NULL. */

@@ -68,7 +68,8 @@ struct NskRing {                      // host-mapped pinned memory
     uint64_t doorbell[kNskSlots];     // = seq when request seq is posted (host store or cuStreamWriteValue64)
     uint64_t done[kNskSlots];         // = seq when request seq has completed (NSK store, system scope)
     uint64_t posted;                  // highest seq the host has handed out (idle watchdog guard)
-    uint64_t pad[7];
+    uint64_t exiting;                 // != 0: the NSK announced its idle exit while waiting for this seq
+    uint64_t pad[6];
     NskReq req[kNskSlots];
 };
 
@@ -95,6 +96,17 @@ struct KeyedArgs {
     uint32_t *status;                // set to nonzero if a page names an unset / other-size key
 };
 
+// Block pairs move with 256-bit global loads/stores (ld/st.global.v8.u32),
+// which need 32-byte alignment; kg.h promises only 16.  So the two-block
+// ("wide") kernel variants run only when m is even and the pointers the
+// kernel receives are 32-byte aligned; otherwise the one-block-per-lane
+// variants (128-bit accesses) run.  Page offsets keep the alignment (m even:
+// page_bytes is a multiple of 32), so one check per batch covers its chunks
+// and texture windows.  nullptr (= a staging slot, cudaMalloc-aligned) passes.
+inline bool wide_ok(uint32_t m, const void *in, const void *out) {
+    return (m & 1u) == 0 && ((((uintptr_t)in) | ((uintptr_t)out)) & 31u) == 0;
+}
+
 // kg_tables.cpp
 void build_base_tables(BaseTables *t);
 int expand_key(const uint8_t *key, int key_bytes, RoundKeys *enc, RoundKeys *dec);  // returns Nr or -1
@@ -109,11 +121,11 @@ cudaError_t launch_pages_keyed(int dir, int mode, int nr, const LaunchArgs &a, c
 // True if a keyed launch of this shape reads its round keys from the
 // constant-bank copy, which load_const_keys must have filled (in stream order)
 // from the snapshot `tab` for direction `dir` before the launch.
-bool keyed_uses_const_keys(int dir, int mode, uint32_t m);
+bool keyed_uses_const_keys(int dir, int mode, uint32_t m, const void *in, const void *out);
 cudaError_t load_const_keys(const DevKeyTable *tab, int dir, cudaStream_t st);
 // True if a keyed launch of this shape has a texture-pipe input variant
 // (LaunchArgs::tex_in honoured).
-bool keyed_takes_tex(int dir, int mode, uint32_t m);
+bool keyed_takes_tex(int dir, int mode, uint32_t m, const void *in, const void *out);
 // Launch the NSK cooperatively with `ctas` CTAs; it expects request seq0 next
 // and exits after idle_ns without a posted request (or on a quit request).
 cudaError_t launch_nsk(NskRing *ring_dev, NskCtl *ctl, uint64_t seq0, uint64_t idle_ns, int ctas, cudaStream_t st);

@@ -915,11 +915,13 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     if (dir == 0 && mode == 0) {
         const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
-        if ((a.m & 1) == 0 && a.tex_in)
+        const bool wide = wide_ok(a.m, a.in, a.out);
+        if (wide && a.tex_in)
             return launch_pdl_tpb(kg_cbc_enc<NR, true, true>, grid, kChainThreads, kSmemEnc, st, a);
-        if ((a.m & 1) == 0) return launch_pdl_tpb(kg_cbc_enc<NR, true>, grid, kChainThreads, kSmemEnc, st, a);
+        if (wide) return launch_pdl_tpb(kg_cbc_enc<NR, true>, grid, kChainThreads, kSmemEnc, st, a);
         return launch_pdl_tpb(kg_cbc_enc<NR, false>, grid, kChainThreads, kSmemEnc, st, a);
-    }    uint64_t want = (nb + 255) / 256;
+    }
+    uint64_t want = (nb + 255) / 256;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
     if (want < 1) want = 1;
@@ -928,12 +930,13 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
         const char *e = getenv("KG_PAIR");
         return (e && *e == '0') ? 0 : 1;
     }();
-    if (pair_ok && (a.m & 1) == 0 && a.tex_in) {
+    const bool wide = pair_ok && wide_ok(a.m, a.in, a.out);
+    if (wide && a.tex_in) {
         if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_blockpar<NR, 1, 0, true, true>, grid, kPairThreads, kSmemDec, st, a);
         if (dir == 1) return launch_pdl_tpb(kg_blockpar<NR, 1, 1, true, true>, grid, kPairThreads, kSmemDec, st, a);
         return launch_pdl_tpb(kg_blockpar<NR, 0, 1, true, true>, grid, kPairThreads, kSmemEnc, st, a);
     }
-    if (pair_ok && (a.m & 1) == 0) {
+    if (wide) {
         if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_blockpar<NR, 1, 0, true>, grid, kPairThreads, kSmemDec, st, a);
         if (dir == 1) return launch_pdl_tpb(kg_blockpar<NR, 1, 1, true>, grid, kPairThreads, kSmemDec, st, a);
         return launch_pdl_tpb(kg_blockpar<NR, 0, 1, true>, grid, kPairThreads, kSmemEnc, st, a);
@@ -964,13 +967,14 @@ cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedA
     if (want < 1) want = 1;
     const unsigned grid = (unsigned)want;
     const int v = keyed_variant();
+    const bool wide = wide_ok(a.m, a.in, a.out);
     if (v > 0 && chain) {
-        if ((a.m & 1) == 0 && a.tex_in)
+        if (wide && a.tex_in)
             return launch_pdl_tpb(kg_keyed_chain<NR, true, true>, grid, kPairThreads, kSmemEnc, st, a, k);
-        if ((a.m & 1) == 0) return launch_pdl_tpb(kg_keyed_chain<NR, true>, grid, kPairThreads, kSmemEnc, st, a, k);
+        if (wide) return launch_pdl_tpb(kg_keyed_chain<NR, true>, grid, kPairThreads, kSmemEnc, st, a, k);
         return launch_pdl_tpb(kg_keyed_chain<NR, false>, grid, kPairThreads, kSmemEnc, st, a, k);
     }
-    if (v > 0 && (a.m & 1) == 0) {
+    if (v > 0 && wide) {
         if (v == 2 && a.tex_in) {
             if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 0, true, true>, grid, kPairThreads, kSmemDec, st, a, k);
             if (dir == 1) return launch_pdl_tpb(kg_keyed_pair<NR, 1, 1, true, true>, grid, kPairThreads, kSmemDec, st, a, k);
@@ -993,12 +997,12 @@ cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedA
 
 }  // namespace
 
-bool keyed_uses_const_keys(int dir, int mode, uint32_t m) {
-    return keyed_variant() == 2 && !(dir == 0 && mode == 0) && (m & 1) == 0;
+bool keyed_uses_const_keys(int dir, int mode, uint32_t m, const void *in, const void *out) {
+    return keyed_variant() == 2 && !(dir == 0 && mode == 0) && wide_ok(m, in, out);
 }
 
-bool keyed_takes_tex(int dir, int mode, uint32_t m) {
-    return (m & 1) == 0 && ((dir == 0 && mode == 0) ? keyed_variant() > 0 : keyed_variant() == 2);
+bool keyed_takes_tex(int dir, int mode, uint32_t m, const void *in, const void *out) {
+    return wide_ok(m, in, out) && ((dir == 0 && mode == 0) ? keyed_variant() > 0 : keyed_variant() == 2);
 }
 
 cudaError_t load_const_keys(const DevKeyTable *tab, int dir, cudaStream_t st) {

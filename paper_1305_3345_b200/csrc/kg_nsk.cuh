@@ -27,7 +27,9 @@
 //  * round keys change per request, so they sit in shared memory and are
 //    read as one broadcast LDS.128 per round;
 //  * idle watchdog: without a posted request for idle_ns (and no request
-//    handed out but not yet rung -- NskRing::posted), the kernel exits; the
+//    handed out but not yet rung -- NskRing::posted), the kernel exits after
+//    a store/fence/load handshake on NskRing::exiting vs ::posted that the
+//    host mirrors (so a request posted during the exit is never lost); the
 //    host relaunches it on the next submit.  Process exit also ends it.
 
 constexpr int kSmemNsk = 3 * kRegion + 16 * 16;  // tables + 15 round keys (uint4)
@@ -45,6 +47,10 @@ __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t *p) {
 __device__ __forceinline__ void st_release_sys_u64(uint64_t *p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sc_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -180,8 +186,18 @@ __global__ void __launch_bounds__(kThreads, 1) kg_nsk(NskRing *ring, NskCtl *ctl
                 uint64_t t0 = globaltimer_ns();
                 while (ld_acquire_sys_u64(&ring->doorbell[slot]) != seq) {
                     if (globaltimer_ns() - t0 > idle_ns) {
+                        // Idle exit handshake with the host (Dekker): announce the
+                        // exit, fence, then re-read `posted`.  The host stores
+                        // `posted`, fences, then reads `exiting` (nsk_post), so at
+                        // least one side sees the other's store: either this
+                        // thread sees the new request and stays, or the host sees
+                        // the announcement and relaunches after this grid ends.
+                        st_relaxed_sys_u64(&ring->exiting, seq);
+                        fence_sc_sys();
                         if (ld_acquire_sys_u64(&ring->posted) >= seq) {
-                            t0 = globaltimer_ns();  // handed out, doorbell pending: keep waiting
+                            st_relaxed_sys_u64(&ring->exiting, 0);  // handed out, doorbell pending: stay
+                            fence_sc_sys();
+                            t0 = globaltimer_ns();
                         } else {
                             quit = 1;
                             break;

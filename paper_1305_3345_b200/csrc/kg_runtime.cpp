@@ -168,6 +168,7 @@ struct Ctx {
     uint64_t ckeys_version = 0;
     int ckeys_dir = -1;
     UseSet ckeys_users;
+    cudaEvent_t ckeys_ready = nullptr;                 // recorded after the last constant-bank (re)fill
     uint32_t *status = nullptr;                        // pinned mapped, kStatusSlots words
     uint32_t *status_dev = nullptr;
     bool status_busy[kStatusSlots] = {};
@@ -251,6 +252,25 @@ int cuda_fail(cudaError_t e, const char *where) {
         cudaError_t _e = (call);                                     \
         if (_e != cudaSuccess) return cuda_fail(_e, #call);          \
     } while (0)
+
+// Every entry point that touches CUDA runs with the context's device
+// current on the calling thread (a thread other than kg_init's may have
+// another device current) and restores the caller's device on return.
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (g.device < 0) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != g.device) cudaSetDevice(g.device);
+        else prev = -1;  // nothing to restore
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 cudaEvent_t take_event() {
     if (!g.ev_pool.empty()) {
@@ -491,6 +511,18 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     int rc = ensure_staging(chunk_pages * page_bytes, need_iv ? chunk_pages * 16 : 16);
     if (rc != KG_OK) return rc;
 
+    // Device-memory input read through the texture pipe: ONE texture over the
+    // whole batch input, each chunk's launch indexing its slice (a texture per
+    // chunk would miss the cache every chunk and evict through host waits).
+    // Batches beyond one texture's reach fall back to a texture per chunk.
+    const uint32_t m = page_bytes / 16;
+    const void *k_out = (kout == K_HOST) ? nullptr : out;  // kernel output: staging slot (aligned) or `out`
+    const bool takes_tex = kin != K_HOST && (keyed ? kg::keyed_takes_tex(dir, mode, m, in, k_out)
+                                                   : kg::wide_ok(m, in, k_out));
+    kg::LaunchArgs batch_tex;
+    Ctx::TexEnt *batch_te = nullptr;
+    if (takes_tex && (rc = tex_for(in, n_pages * page_bytes, &batch_tex, &batch_te)) != KG_OK) return rc;
+
     KG_CU(cudaEventRecord(g.ev_begin, st));
     trace(0, 'b', st);
     KG_CU(cudaStreamWaitEvent(g.s_h2d, g.ev_begin, 0));
@@ -588,19 +620,22 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         a.m = page_bytes / 16;
         a.in_place = (const void *)a.in == (const void *)a.out;
         a.rk = rk;
+        Ctx::TexEnt *te = nullptr;
+        if (batch_te) {
+            a.tex_in = batch_tex.tex_in;
+            a.tex_off = batch_tex.tex_off + (int64_t)(off / 16);
+        } else if (takes_tex && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) {
+            return rc;
+        }
         if (keyed) {
             kg::KeyedArgs k = *keyed;
             k.key_ids += p0;
-            Ctx::TexEnt *te = nullptr;
-            if (kg::keyed_takes_tex(dir, mode, a.m) && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
             const int sms = g.nsk.on ? (g.num_sms - g.nsk.ctas > 0 ? g.num_sms - g.nsk.ctas : 1) : g.num_sms;
             cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, g.s_comp);
             if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
             g_launches.fetch_add(1, std::memory_order_relaxed);
             if (te) KG_CU(te->use.record(g.s_comp));
         } else {
-            Ctx::TexEnt *te = nullptr;
-            if ((a.m & 1) == 0 && (rc = tex_for(a.in, nbytes, &a, &te)) != KG_OK) return rc;
             rc = launch(dir, mode, nr, a, g.s_comp);
             if (rc != KG_OK) return rc;
             if (te) KG_CU(te->use.record(g.s_comp));
@@ -610,6 +645,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         if (!lag && (rc = d2h(i, p0)) != KG_OK) return rc;
     }
     if (lag && (rc = d2h(sched.size() - 1, p_prev)) != KG_OK) return rc;
+    if (batch_te) KG_CU(batch_te->use.record(g.s_comp));
     if (iv_upfront) KG_CU(cudaEventRecord(g.iv_free[ivb], g.s_comp));
     // join: the caller's stream continues after the last D2H
     KG_CU(cudaEventRecord(g.ev_begin, g.s_d2h));
@@ -628,6 +664,7 @@ inline void cpu_relax() {
 }
 
 int nsk_launch(uint64_t seq0) {
+    vstore(&g.nsk.ring->exiting, 0);  // the previous grid (if any) has ended
     KG_CU(cudaMemsetAsync(g.nsk.ctl, 0, sizeof(kg::NskCtl), g.nsk.st));
     KG_CU(kg::launch_nsk(g.nsk.ring_dev, g.nsk.ctl, seq0, g.nsk.idle_ns, g.nsk.ctas, g.nsk.st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -683,6 +720,21 @@ int64_t nsk_post(uint32_t op, const void *in, void *out, const void *ivs, uint64
     memcpy((void *)&g.nsk.ring->req[slot], &r, sizeof r);
     vstore(&g.nsk.ring->posted, seq);
     std::atomic_thread_fence(std::memory_order_seq_cst);
+    // Idle-exit handshake (kg_nsk.cuh): if the kernel announced its exit, it
+    // either re-read `posted` after our store and stays (it clears the flag),
+    // or it exits without this request: then wait for the grid to end and
+    // relaunch it expecting `seq`.
+    for (uint64_t spin = 0; vload(&g.nsk.ring->exiting) != 0; ++spin) {
+        cudaError_t e = cudaStreamQuery(g.nsk.st);
+        if (e == cudaSuccess) {
+            rc = nsk_launch(seq);
+            if (rc != KG_OK) return rc;
+            break;
+        }
+        if (e != cudaErrorNotReady) return cuda_fail(e, "NSK died");
+        cudaGetLastError();
+        cpu_relax();
+    }
     g.nsk.seq = seq;
     if (direct) {
         vstore(&g.nsk.ring->doorbell[slot], seq);
@@ -823,6 +875,7 @@ int kg_init(int device) {
 
 int kg_set_pipeline(uint64_t chunk_bytes, int slots) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     if ((chunk_bytes != 0 && chunk_bytes < 16) || slots < 2 || slots > kMaxSlots) return KG_EINVAL;
     if (slots != g.n_slots) {
@@ -879,6 +932,7 @@ bool local_cpus(int device, cpu_set_t *set) {
 
 void *kg_alloc_pinned(uint64_t bytes) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up || bytes == 0) return nullptr;
     cpu_set_t local;
     const bool have_local = local_cpus(g.device, &local);
@@ -937,6 +991,7 @@ void *kg_alloc_pinned(uint64_t bytes) {
 
 int kg_free_pinned(void *p) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     auto it = g_pinned.find(p);
     if (it == g_pinned.end()) return KG_EINVAL;
     if (it->second == 0) {
@@ -981,6 +1036,7 @@ int kg_set_key(int key_id, const uint8_t *key, int key_bytes) {
 int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n_pages, uint32_t page_bytes,
                         const void *ivs, int key_id, void *stream) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     if ((dir != KG_ENCRYPT && dir != KG_DECRYPT) || (mode != KG_MODE_CBC && mode != KG_MODE_ECB)) return KG_EINVAL;
     if (n_pages == 0 || page_bytes == 0 || page_bytes % 16 != 0) return KG_EINVAL;
@@ -1038,7 +1094,7 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
         a.m = page_bytes / 16;
         a.in_place = (in == out);
         a.rk = rk;
-        if (kin == K_DEVICE && (a.m & 1) == 0) rc = launch_tex(dir, mode, ks.nr, a, page_bytes, st);
+        if (kin == K_DEVICE && kg::wide_ok(a.m, a.in, a.out)) rc = launch_tex(dir, mode, ks.nr, a, page_bytes, st);
         else rc = launch(dir, mode, ks.nr, a, st);
     } else {
         rc = submit_staged(dir, mode, ks.nr, rk, (const uint8_t *)in, kin, (uint8_t *)out, kout, n_pages,
@@ -1065,6 +1121,7 @@ static int keyed_setup() {
         if (cudaEventCreateWithFlags(&g.ktab_ready[i], cudaEventDisableTiming) != cudaSuccess) goto fail;
         g.ktab_dev_version[i] = 0;
     }
+    if (cudaEventCreateWithFlags(&g.ckeys_ready, cudaEventDisableTiming) != cudaSuccess) goto fail;
     if (cudaHostAlloc((void **)&g.status, kStatusSlots * sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess) goto fail;
     if (cudaHostGetDevicePointer((void **)&g.status_dev, g.status, 0) != cudaSuccess) goto fail;
     memset(g.status, 0, kStatusSlots * sizeof(uint32_t));
@@ -1090,6 +1147,8 @@ static void keyed_teardown() {
     g.status = g.status_dev = nullptr;
     g.ktab_cur = -1;
     g.ckeys_users.reset();
+    if (g.ckeys_ready) cudaEventDestroy(g.ckeys_ready);
+    g.ckeys_ready = nullptr;
     g.ckeys_version = 0;
     g.ckeys_dir = -1;
     for (auto &b : g.status_busy) b = false;
@@ -1119,6 +1178,7 @@ static int keyed_snapshot(cudaStream_t st, const kg::DevKeyTable **out) {
 int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint64_t n_pages, uint32_t page_bytes,
                               const void *ivs, const uint16_t *key_ids, int key_bytes, void *stream) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     if ((dir != KG_ENCRYPT && dir != KG_DECRYPT) || (mode != KG_MODE_CBC && mode != KG_MODE_ECB)) return KG_EINVAL;
     if (n_pages == 0 || page_bytes == 0 || page_bytes % 16 != 0) return KG_EINVAL;
@@ -1181,16 +1241,24 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
     // keyed batches always launch; while the NSK holds SMs they use the others
     // (a grid wider than the free SMs would wait behind the resident NSK forever)
     const int sms = g.nsk.on ? (g.num_sms - g.nsk.ctas > 0 ? g.num_sms - g.nsk.ctas : 1) : g.num_sms;
-    const bool ck = kg::keyed_uses_const_keys(dir, mode, a.m);
+    // the pointers the kernels receive: staging slots (nullptr: aligned) for host memory when staged
+    const void *k_in = staged && kin == K_HOST ? nullptr : zin;
+    const void *k_out = staged && kout == K_HOST ? nullptr : zout;
+    const bool ck = kg::keyed_uses_const_keys(dir, mode, a.m, k_in, k_out);
     if (ck && (g.ckeys_version != g.ktab_dev_version[g.ktab_cur] || g.ckeys_dir != dir)) {
         // refill the constant-bank copy behind every launch still reading it
         KG_CU(g.ckeys_users.stream_wait(st));
         g.ckeys_users.reset();
         g.ckeys_version = 0;
         KG_CU(kg::load_const_keys(tab, dir, st));
+        KG_CU(cudaEventRecord(g.ckeys_ready, st));
         g.ckeys_version = g.ktab_dev_version[g.ktab_cur];
         g.ckeys_dir = dir;
     }
+    // every launch reading the constant-bank copy waits for its (re)fill, which
+    // may still be queued on another stream (waiting on an event of the same
+    // stream is free)
+    if (ck) KG_CU(cudaStreamWaitEvent(st, g.ckeys_ready, 0));
     if (staged) {
         // chunk launches run on the internal compute stream, forked from and
         // joined back onto `st`: the snapshot / constant-key uses are
@@ -1201,7 +1269,7 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
         KG_CU(g.ktab_used[g.ktab_cur].record(st));
     } else {
         Ctx::TexEnt *te = nullptr;
-        if (kin == K_DEVICE && kg::keyed_takes_tex(dir, mode, a.m) && (rc = tex_for(zin, total, &a, &te)) != KG_OK)
+        if (kin == K_DEVICE && kg::keyed_takes_tex(dir, mode, a.m, k_in, k_out) && (rc = tex_for(zin, total, &a, &te)) != KG_OK)
             return rc;
         cudaError_t e = kg::launch_pages_keyed(dir, mode, nr, a, k, sms, st);
         if (e != cudaSuccess) return cuda_fail(e, "launch_pages_keyed");
@@ -1288,6 +1356,7 @@ int kg_wait(int64_t ticket) {
 
 int kg_poll(int64_t ticket) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     auto it = g.tickets.find(ticket);
     if (it == g.tickets.end() || it->second.claimed) return KG_ETICKET;
@@ -1303,6 +1372,7 @@ int kg_poll(int64_t ticket) {
 
 int kg_nsk_start(int ctas, int flags, uint32_t idle_ms) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     if (flags & ~KG_NSK_DIRECT) return KG_EINVAL;
     if (ctas == 0) ctas = 16;
@@ -1415,6 +1485,7 @@ int nsk_calibrate(uint64_t *chosen) {
 
 int kg_nsk_dispatch(uint64_t max_bytes, uint64_t *chosen) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     if (!g.nsk.on) return KG_EINVAL;
     if (max_bytes == 0) return nsk_calibrate(chosen);
@@ -1425,15 +1496,26 @@ int kg_nsk_dispatch(uint64_t max_bytes, uint64_t *chosen) {
 
 int kg_nsk_stop(void) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     return nsk_stop_locked();
 }
 
 int kg_shutdown(void) {
     std::lock_guard<std::mutex> lk(g_mu);
+    DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     nsk_stop_locked();
-    cudaDeviceSynchronize();
+    // An asynchronous fault (KG_ECUDA from kg_wait) leaves a sticky error: the
+    // primary context is unusable until it is reset.  Detect it (a second
+    // synchronize still fails after clearing the last error) and reset the
+    // device at the end, so that kg_init can start over in a fresh context.
+    bool sticky = false;
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        sticky = cudaDeviceSynchronize() != cudaSuccess;
+        cudaGetLastError();
+    }
     keyed_teardown();
     for (auto &kv : g.tickets)
         if (kv.second.ev) cudaEventDestroy(kv.second.ev);
@@ -1461,6 +1543,12 @@ int kg_shutdown(void) {
     g.ev_begin = nullptr;
     g.s_h2d = g.s_comp = g.s_d2h = nullptr;
     for (auto &k : g.keys) k = KeySlot();
+    if (sticky) {
+        cudaDeviceReset();       // also releases cudaHostAlloc'd / registered host memory of the context
+        for (auto &kv : g_pinned)
+            if (kv.second != 0) munmap(kv.first, kv.second);
+        g_pinned.clear();
+    }
     g.up = false;
     g.device = -1;
     cudaGetLastError();

@@ -88,3 +88,17 @@ def test_example_links_against_the_library(tmp_path):
                            "-lkgpu", f"-Wl,-rpath,{os.path.dirname(kg.LIB_PATH)}", "-o", str(exe)])
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 2 and "usage" in out.stderr
+
+
+def test_enotsup_without_a_device():
+    """kg_init on a process that sees no CUDA device -> KG_ENOTSUP (the
+    library still loads; no compute call is made)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import paper_1305_3345_b200 as kg; "
+            "print(kg.raw_lib().kg_init(0))" % ROOT)
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    import paper_1305_3345_b200 as kg
+    assert int(r.stdout.strip().splitlines()[-1]) == kg.ENOTSUP

@@ -108,3 +108,106 @@ def test_shutdown_and_reinit():
     x = torch.zeros(4096, dtype=torch.uint8, device="cuda")
     iv = torch.zeros(16, dtype=torch.uint8, device="cuda")
     assert kg.submit_pages_raw(0, 0, x, x, 1, 4096, iv, 3) == kg.ENOKEY   # keys forgotten
+
+
+def test_eagain_ticket_table_full():
+    """KG_MAX_INFLIGHT unretired tickets: the next submit returns KG_EAGAIN
+    (SPEC.md:51 QueueFull) and enqueues nothing; waiting on the oldest frees
+    a slot."""
+    kg, torch = kg_ready()
+    kg.set_key(0, synth.make_key(16))
+    x = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    y = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    l0 = kg.launch_count()
+    ts = [kg.submit_pages(1, 1, x, y, 1, 16, None, 0) for _ in range(kg.MAX_INFLIGHT)]
+    launched = kg.launch_count() - l0
+    assert kg.submit_pages_raw(1, 1, x, y, 1, 16, None, 0) == kg.EAGAIN
+    assert kg.launch_count() - l0 == launched                  # nothing enqueued
+    kg.wait(ts[0])
+    t = kg.submit_pages(1, 1, x, y, 1, 16, None, 0)
+    assert t > ts[-1]
+    for tk in ts[1:] + [t]:
+        kg.wait(tk)
+
+
+def test_enomem_staging_then_recovers():
+    """The device staging ring cannot be allocated -> KG_ENOMEM, nothing
+    written; once memory is free again the same batch succeeds."""
+    kg, torch = kg_ready()
+    key = synth.make_key(16)
+    kg.set_key(0, key)
+    n, pb = 4096, 4096
+    data = synth.make_pages(n, pb, seed=90)
+    ivs = synth.make_ivs(n, seed=91)
+    hx = torch.from_numpy(data).pin_memory()
+    hiv = torch.from_numpy(ivs).pin_memory()
+    hout = torch.zeros(n * pb, dtype=torch.uint8).pin_memory()
+    kg.set_host_path(kg.HOST_STAGED, 0)
+    kg.set_pipeline(n * pb, 3)                     # slot count changes: the ring is freed and re-allocated on use
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    hog = torch.empty(free - (24 << 20), dtype=torch.uint8, device="cuda")   # leave < 3 x 16 MiB
+    try:
+        assert kg.submit_pages_raw(1, 0, hx, hout, n, pb, hiv, 0) == kg.ENOMEM
+        assert int(hout.sum()) == 0                # nothing written
+    finally:
+        del hog
+        torch.cuda.empty_cache()
+    try:
+        kg.wait(kg.submit_pages(1, 0, hx, hout, n, pb, hiv, 0))
+    finally:
+        kg.set_pipeline(0, 4)
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)
+    from gpu_util import oracle_pages
+    assert np.array_equal(hout.numpy(), oracle_pages(1, 0, key, data, n, pb, ivs))
+
+
+_FAULT = r"""
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import torch
+import paper_1305_3345_b200 as kg
+import oracle, synth
+torch.cuda.set_device(0)
+kg.init(0)
+kg.set_key(0, synth.make_key(16))
+small = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+torch.cuda.synchronize()
+# an ECB batch that runs 3 GiB past a 1 MiB allocation (48-byte pages: plain loads)
+t = kg.submit_pages(1, 1, small, small, 1 << 26, 48, None, 0)
+assert t >= 0
+rc = kg.wait_raw(t)
+print("wait", rc)
+assert rc == kg.ECUDA
+assert kg.submit_pages_raw(1, 1, small, small, 1, 48, None, 0) in (kg.ECUDA, kg.EINVAL)
+lib = kg.raw_lib()
+assert lib.kg_shutdown() == kg.OK          # resets the faulted context
+assert lib.kg_init(0) == kg.OK             # ... and the library starts over
+key = synth.make_key(16, seed=3)
+kg.set_key(0, key)
+n, pb = 8, 4096
+data, ivs = synth.make_pages(n, pb, seed=4), synth.make_ivs(n, seed=5)
+hx, hout, hiv = kg.alloc_pinned(n * pb), kg.alloc_pinned(n * pb), kg.alloc_pinned(16 * n)
+hx.copy_(torch.from_numpy(data)); hiv.copy_(torch.from_numpy(ivs))
+kg.wait(kg.submit_pages(1, 0, hx, hout, n, pb, hiv, 0))     # pinned host: zero-copy launch in the new context
+assert np.array_equal(hout.numpy(), oracle.pages(1, 0, key, data, n, pb, ivs))
+print("recovered")
+sys.stdout.flush()
+os._exit(0)
+"""
+
+
+def test_ecuda_async_fault_then_shutdown_init_recovers(tmp_path):
+    """An asynchronous device fault surfaces as KG_ECUDA at kg_wait;
+    kg_shutdown + kg_init recover (in a subprocess: the fault kills that
+    process's context)."""
+    import os
+    import subprocess
+    import sys
+    kg_ready()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    f = tmp_path / "fault.py"
+    f.write_text(_FAULT)
+    r = subprocess.run([sys.executable, str(f), root], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "recovered" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]

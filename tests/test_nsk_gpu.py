@@ -47,8 +47,7 @@ def test_nsk_parity(nsk, flags, where):
                 exp = oracle_pages(d, mode, key, data, n, pb, ivs if mode == 0 else None)
                 got = run(kg, torch, d, mode, key, data, n, pb, ivs if mode == 0 else None, where)
                 assert first_mismatch(got, exp) is None, (n, pb, kb, d, mode)
-        got = run(kg, torch, 1, 0, key, exp if False else oracle_pages(0, 0, key, data, n, pb, ivs), n, pb, ivs,
-                  where, inplace=True)
+        got = run(kg, torch, 1, 0, key, oracle_pages(0, 0, key, data, n, pb, ivs), n, pb, ivs, where, inplace=True)
         assert np.array_equal(got, data)
 
 
@@ -84,6 +83,53 @@ def test_nsk_idle_exit_and_relaunch(nsk):
         assert np.array_equal(run(kg, torch, 1, 0, key, data, 8, 4096, ivs, "device"), exp)
         time.sleep(0.2)                        # the NSK exits; the next submit relaunches it
     assert kg.launch_count() - l0 >= 2
+
+
+_IDLE_RACE = r"""
+import random, sys, time
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_1305_3345_b200 as kg
+import synth
+flags = int(sys.argv[2])
+torch.cuda.set_device(0)
+kg.init(0)
+kg.set_key(0, synth.make_key(16, seed=5))
+x = torch.from_numpy(synth.make_pages(1, 4096, seed=6)).cuda()
+iv = torch.from_numpy(synth.make_ivs(1, seed=7)).cuda()
+y = torch.empty_like(x)
+ref = torch.empty_like(x)
+kg.wait(kg.submit_pages(1, 0, x, ref, 1, 4096, iv, 0))
+torch.cuda.synchronize()
+kg.nsk_start(2, flags, 1)                 # 1 ms idle watchdog
+rnd = random.Random(11)
+l0 = kg.launch_count()
+for i in range(600):
+    time.sleep(rnd.uniform(0.0006, 0.0016))  # straddle the watchdog
+    kg.wait(kg.submit_pages(1, 0, x, y, 1, 4096, iv, 0))
+torch.cuda.current_stream().synchronize()
+assert torch.equal(y, ref)
+print("relaunches", kg.launch_count() - l0)
+kg.nsk_stop()
+"""
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_nsk_idle_exit_race(tmp_path, flags):
+    """a request posted while the NSK decides to exit on idle must
+    not be lost.  Requests arrive at random gaps around a 1 ms watchdog; every
+    one must complete (run in a subprocess with a timeout: a lost request
+    would spin forever)."""
+    import os
+    import subprocess
+    import sys
+    kg_ready()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "race.py"
+    script.write_text(_IDLE_RACE)
+    r = subprocess.run([sys.executable, str(script), root, str(flags)], capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert int(r.stdout.split("relaunches")[1]) >= 10   # the watchdog really fired between requests
 
 
 def test_nsk_stream_ordering(nsk):
