@@ -7,7 +7,7 @@ PKG     := paper_1305_3345_b200
 CSRC    := $(PKG)/csrc
 LIB     := $(PKG)/libkgpu.so
 
-all: $(LIB) oracle/libkgo.so build/test_kat build/pipes build/latency build/kgpu_crypt
+all: $(LIB) oracle/libkgo.so build/test_kat build/pipes build/latency build/kgpu_crypt build/e1
 
 build:
 	mkdir -p build
@@ -34,6 +34,10 @@ build/pipes: tools/pipes.cu | build
 
 build/latency: tools/latency.cu include/kg.h $(LIB) | build
 	$(NVCC) -O2 -std=c++17 $(ARCH) -Iinclude -o $@ $< -L$(PKG) -lkgpu -Xlinker -rpath,'$$ORIGIN/../$(PKG)'
+
+# the paper's §3.1 E1 experiment: launch vs CUDA graph vs persistent kernel at 512/1024/2048 threads
+build/e1: tools/e1.cu | build
+	$(NVCC) -O2 -std=c++17 $(ARCH) -o $@ $<
 
 build/kgpu_crypt: examples/kgpu_crypt.c include/kg.h $(LIB) | build
 	gcc -std=c99 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lkgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)'

@@ -184,7 +184,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, pci_bus_id=None, index=0, period=0.001):
+    def __init__(self, pci=None, index=0, period=0.001):
         self.ok = False
         self.samples, self.reasons = [], set()
         self.period = period
@@ -193,12 +193,13 @@ class ClockSampler:
             pynvml.nvmlInit()
             self.nv = pynvml
             self.h = None
-            if pci_bus_id:
-                try:
-                    self.h = pynvml.nvmlDeviceGetHandleByPciBusId(pci_bus_id.encode() if isinstance(pci_bus_id, str)
-                                                                   else pci_bus_id)
-                except Exception:  # noqa: BLE001
-                    self.h = None
+            if pci is not None:  # (domain, bus, device) of the CUDA device: NVML ignores CUDA_VISIBLE_DEVICES
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    p = pynvml.nvmlDeviceGetPciInfo(h)
+                    if (p.domain, p.bus, p.device) == tuple(pci):
+                        self.h = h
+                        break
             if self.h is None:
                 self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
@@ -409,7 +410,8 @@ class Ctx:
             self.comm = {"backend": dist.get_backend(), "world": dist.get_world_size(),
                          "allreduce_sum_of_ones": int(one.item())}
         try:
-            self.pci = torch.cuda.get_device_properties(self.dev).pci_bus_id
+            pr = torch.cuda.get_device_properties(self.dev)
+            self.pci = (int(pr.pci_domain_id), int(pr.pci_bus_id), int(pr.pci_device_id))
         except Exception:  # noqa: BLE001
             self.pci = None
 

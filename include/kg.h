@@ -77,8 +77,8 @@ extern "C" {
 #define KG_ENOTINIT -3  /* kg_init not called (or after kg_shutdown)          */
 #define KG_EAGAIN   -4  /* ticket table full: wait on an older ticket first   */
 #define KG_ENOMEM   -5  /* device staging allocation failed                   */
-#define KG_ECUDA    -6  /* CUDA runtime/driver error (sticky: kg_shutdown +   */
-                        /* kg_init to recover)                                */
+#define KG_ECUDA    -6  /* CUDA runtime/driver error; after an asynchronous   */
+                        /* fault the process's context is dead (kg_shutdown) */
 #define KG_ENOTSUP  -7  /* unsupported (e.g. no sm_100 device)                */
 #define KG_ETICKET  -8  /* unknown, retired or already-claimed ticket         */
 
@@ -148,13 +148,13 @@ KG_API int kg_wait(int64_t ticket);
 KG_API int kg_poll(int64_t ticket);
 
 /* Drain all outstanding work, free the staging ring, streams, events and
- * tables, forget all keys.  After an
- * asynchronous device fault (KG_ECUDA from kg_wait/kg_poll: a sticky CUDA
- * error) it also resets the device (cudaDeviceReset), so that kg_init can
- * start again in a fresh context -- every allocation the process made on
- * that device (the caller's and kg_alloc_pinned buffers included) is gone
- * then.  KG_ENOTINIT if not
- * initialised. */
+ * tables, forget all keys.  KG_ENOTINIT if not initialised.
+ * After an asynchronous device fault (KG_ECUDA from kg_wait/kg_poll) the
+ * CUDA context of the process is unusable -- CUDA's sticky errors end only
+ * with the process ("the process must be terminated and relaunched",
+ * cudaErrorIllegalAddress et al.): kg_shutdown still succeeds and releases
+ * the host-side state, a later kg_init returns KG_ECUDA, and a new process
+ * starts cleanly (tests/test_errors_gpu.py). */
 KG_API int kg_shutdown(void);
 
 /* Static description of a status code; never NULL. */

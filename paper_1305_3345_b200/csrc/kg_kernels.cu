@@ -60,18 +60,36 @@ __device__ unsigned long long g_stamps[148 * 34];
 
 __device__ __forceinline__ uint32_t rotl32(uint32_t v, int s) { return __funnelshift_l(v, v, s); }
 
-// Replicate the 256-entry base tables into the lane-private layout.
+// Replicate the 256-entry base tables into the lane-private layout.  Warp w
+// owns entries [w*per, (w+1)*per): its lanes fetch them with ONE coalesced
+// load per table (all loads in flight at once), then the warp writes the 32
+// lane replicas of one entry per step (entry broadcast by SHFL; lane l
+// stores to bank l: conflict-free STS).  A per-thread strided loop over the
+// 8192 (entry, lane) pairs instead serialised ~16 dependent global loads per
+// thread (a 3.7 us prologue, profiles/r1_tail); this one is about one load
+// latency plus 5*per STS per warp.
 template <bool DEC>
 __device__ __forceinline__ void fill_tables(char *sm) {
-    for (int idx = threadIdx.x; idx < 256 * 32; idx += blockDim.x) {
-        const int x = idx >> 5, l = idx & 31;
-        const uint32_t v = DEC ? g_tables.td0[x] : g_tables.te0[x];
-        const int o = x * 256 + l * 4;
-        *reinterpret_cast<uint32_t *>(sm + o) = v;
-        *reinterpret_cast<uint32_t *>(sm + o + 128) = rotl32(v, 8);
-        *reinterpret_cast<uint32_t *>(sm + kRegion + o) = rotl32(v, 16);
-        *reinterpret_cast<uint32_t *>(sm + kRegion + o + 128) = rotl32(v, 24);
-        if (DEC) *reinterpret_cast<uint32_t *>(sm + 2 * kRegion + o) = g_tables.isb4[x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int per = (256 + nw - 1) / nw;  // <= 32 for blockDim >= 256 (every kernel here)
+    const int x0 = warp * per;
+    const int xl = x0 + lane;
+    const bool mine = lane < per && xl < 256;
+    const uint32_t v_l = mine ? (DEC ? g_tables.td0[xl] : g_tables.te0[xl]) : 0u;
+    const uint32_t s_l = (DEC && mine) ? g_tables.isb4[xl] : 0u;
+#pragma unroll 4
+    for (int k = 0; k < per; ++k) {
+        const uint32_t v = __shfl_sync(0xffffffffu, v_l, k);
+        const uint32_t sb = DEC ? __shfl_sync(0xffffffffu, s_l, k) : 0u;
+        const int x = x0 + k;
+        if (x < 256) {
+            const int o = x * 256 + lane * 4;
+            *reinterpret_cast<uint32_t *>(sm + o) = v;
+            *reinterpret_cast<uint32_t *>(sm + o + 128) = rotl32(v, 8);
+            *reinterpret_cast<uint32_t *>(sm + kRegion + o) = rotl32(v, 16);
+            *reinterpret_cast<uint32_t *>(sm + kRegion + o + 128) = rotl32(v, 24);
+            if (DEC) *reinterpret_cast<uint32_t *>(sm + 2 * kRegion + o) = sb;
+        }
     }
 }
 

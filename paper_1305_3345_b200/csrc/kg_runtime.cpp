@@ -318,7 +318,7 @@ int ensure_staging(uint64_t bytes, uint64_t ivb) {
     return KG_OK;
 }
 
-enum Kind { K_BAD = 0, K_DEVICE = 1, K_HOST = 2 };
+enum Kind { K_BAD = 0, K_DEVICE = 1, K_HOST = 2, K_ERR = 3 /* the CUDA context itself failed */ };
 
 // Classify a caller pointer; for pinned host memory also return the address
 // a kernel may use to reach it over the host link (UVA: usually identical).
@@ -327,7 +327,7 @@ Kind classify(const void *p, const void **dev_alias = nullptr) {
     cudaError_t e = cudaPointerGetAttributes(&at, p);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        return K_BAD;
+        return e == cudaErrorInvalidValue ? K_BAD : K_ERR;
     }
     switch (at.type) {
         case cudaMemoryTypeDevice:
@@ -1055,6 +1055,7 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
     const void *zin = in, *zout = out, *ziv = ivs;
     const Kind kin = classify(in, &zin), kout = classify(out, &zout),
                kiv = need_iv ? classify(ivs, &ziv) : K_DEVICE;
+    if (kin == K_ERR || kout == K_ERR || kiv == K_ERR) return KG_ECUDA;
     if (kin == K_BAD || kout == K_BAD || kiv == K_BAD) return KG_EINVAL;
     if (g.tickets.size() >= (size_t)KG_MAX_INFLIGHT) return KG_EAGAIN;
 
@@ -1195,6 +1196,7 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
     const void *zin = in, *zout = out, *ziv = ivs, *zid = key_ids;
     const Kind kin = classify(in, &zin), kout = classify(out, &zout), kid = classify(key_ids, &zid),
                kiv = need_iv ? classify(ivs, &ziv) : K_DEVICE;
+    if (kin == K_ERR || kout == K_ERR || kiv == K_ERR || kid == K_ERR) return KG_ECUDA;
     if (kin == K_BAD || kout == K_BAD || kiv == K_BAD || kid == K_BAD) return KG_EINVAL;
     // The ids are read by the kernels wherever they live (device memory or the
     // device alias of pinned memory).  Batches touching host memory follow the
@@ -1506,16 +1508,10 @@ int kg_shutdown(void) {
     DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
     nsk_stop_locked();
-    // An asynchronous fault (KG_ECUDA from kg_wait) leaves a sticky error: the
-    // primary context is unusable until it is reset.  Detect it (a second
-    // synchronize still fails after clearing the last error) and reset the
-    // device at the end, so that kg_init can start over in a fresh context.
-    bool sticky = false;
-    if (cudaDeviceSynchronize() != cudaSuccess) {
-        cudaGetLastError();
-        sticky = cudaDeviceSynchronize() != cudaSuccess;
-        cudaGetLastError();
-    }
+    // After an asynchronous fault the context is dead (sticky error): the
+    // frees below fail harmlessly and only the host-side state is reset.
+    cudaDeviceSynchronize();
+    cudaGetLastError();
     keyed_teardown();
     for (auto &kv : g.tickets)
         if (kv.second.ev) cudaEventDestroy(kv.second.ev);
@@ -1543,12 +1539,6 @@ int kg_shutdown(void) {
     g.ev_begin = nullptr;
     g.s_h2d = g.s_comp = g.s_d2h = nullptr;
     for (auto &k : g.keys) k = KeySlot();
-    if (sticky) {
-        cudaDeviceReset();       // also releases cudaHostAlloc'd / registered host memory of the context
-        for (auto &kv : g_pinned)
-            if (kv.second != 0) munmap(kv.first, kv.second);
-        g_pinned.clear();
-    }
     g.up = false;
     g.device = -1;
     cudaGetLastError();

@@ -28,7 +28,9 @@ def _run(args, extra_env=None, timeout=900):
 
 def _check_config(c, n_gpus):
     assert c["value"] > 0 and c["check"]["mismatched_pages"] == 0
-    assert c["check"]["pages"] == c["n_pages_per_gpu"] * n_gpus if c["scaling"] == "weak" else True
+    per_gpu = c["n_pages_per_gpu"] if "n_pages_per_gpu" in c else c["config"]["n_pages_per_gpu"]
+    if c["scaling"] == "weak":
+        assert c["check"]["pages"] == per_gpu * n_gpus
     assert 0 < c["roofline"]["frac"] < 1.05
     assert c["gpu_launches"] >= c["steps"] * n_gpus
 
