@@ -694,7 +694,7 @@ def c4_sweep(ctx, args):
                 f()
             row[f"{name}_us"] = round(lat(f, reps), 2)
         if n <= args.sweep_nsk_pages:
-            kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+            kg.nsk_start(16, kg.NSK_DIRECT | kg.NSK_NOCAL, 5000)
 
             def g():
                 kg.wait(kg.submit_pages(1, 0, dx, dout, n, PB, div, 0, s))

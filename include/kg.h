@@ -222,21 +222,46 @@ KG_API int kg_set_host_path(int mode, uint64_t zc_max_bytes);
  * KG_ENOMEM; KG_ECUDA.  kg_nsk_stop drains and stops it (KG_OK if not
  * running); kg_shutdown stops it too. */
 #define KG_NSK_DIRECT 1
+#define KG_NSK_NOCAL 2  /* skip the start-up calibration: every request goes to the NSK */
 KG_API int kg_nsk_start(int ctas, int flags, uint32_t idle_ms);
 KG_API int kg_nsk_stop(void);
 
-/* Size-based dispatch while the NSK runs (row f2; the paper's "calibrating
- * the crossover point at boot", between its two GPU paths):
- * requests of at most max_bytes (n_pages*page_bytes) go to the NSK, larger
- * ones are launched as ordinary kernels on the SMs the NSK leaves free (the
- * paper's "switches to a traditional CUDA kernel launch").
- * max_bytes = 0 calibrates: times both paths on 1..8192-page AES-128 decrypt
- * batches in device memory and keeps the largest size where the NSK is not
- * slower (a tie goes to the NSK).  UINT64_MAX = everything to the NSK (the
- * default after kg_nsk_start).  *chosen (may be NULL) receives the threshold.
- * There is no CPU leg: the library has no CPU path by design.
- * Errors: KG_ENOTINIT, KG_EINVAL (NSK not running), KG_ENOMEM, KG_ECUDA. */
+/* Size-based dispatch while the NSK runs (row f2; the paper's "dynamically
+ * dispatching tasks ... depending on their size ... calibrate it using
+ * microbenchmarks at boot time").  The library has no CPU
+ * path (no CPU fallback by design), so the two legs are its two GPU paths:
+ * requests of at most max_bytes (n_pages*page_bytes) go to the NSK (the
+ * low-overhead path for small requests), larger ones are launched as
+ * ordinary kernels on the SMs the NSK leaves free (the paper's "switches to a
+ * traditional CUDA kernel launch").
+ * kg_nsk_start calibrates at start unless KG_NSK_NOCAL is given: it times
+ * both paths, caller-observed, on AES-128-CBC decrypt batches of 1, 2, 4, ...
+ * 4 KiB pages in device memory (median of 5 after 2 warm-ups, stopping two
+ * sizes after the launch first wins) and sets the threshold with
+ * kg_dispatch_threshold.  max_bytes = 0 re-calibrates; UINT64_MAX sends
+ * everything to the NSK; any other value is used as given.  *chosen (may be
+ * NULL) receives the threshold.  Errors: KG_ENOTINIT, KG_EINVAL (NSK not
+ * running), KG_ENOMEM, KG_ECUDA. */
 KG_API int kg_nsk_dispatch(uint64_t max_bytes, uint64_t *chosen);
+
+/* One calibration sample: batch size and the two paths' median latencies. */
+typedef struct {
+    uint64_t bytes;
+    double nsk_us;
+    double launch_us;
+} kg_calib_point;
+
+/* The dispatch rule (pure; no device needed): given samples sorted by size,
+ * the threshold is the size of the last sample before the first one where
+ * the launch is strictly faster (a tie goes to the NSK, the small-request
+ * path, SPEC.md:414's tie rule); 0 if the launch wins at the first sample;
+ * UINT64_MAX if it never wins (or n <= 0).  Dispatch is then monotone by
+ * construction: NSK for sizes <= threshold, launches above. */
+KG_API uint64_t kg_dispatch_threshold(const kg_calib_point *pts, int n);
+
+/* Copy up to max_pts samples of the last calibration into pts; returns the
+ * number of samples it has (0 if none yet).  Errors: KG_ENOTINIT, KG_EINVAL. */
+KG_API int kg_nsk_calibration(kg_calib_point *pts, int max_pts);
 
 /* Pinned host allocations for batches (row f4; "allocate memory in the pinned
  * region ... to save an extra copy"): pinned and mapped

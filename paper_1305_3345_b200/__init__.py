@@ -27,8 +27,8 @@ MAX_INFLIGHT = 65536
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
                "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path",
                "kg_nsk_start", "kg_nsk_stop", "kg_nsk_dispatch", "kg_alloc_pinned", "kg_free_pinned",
-               "kg_submit_pages_keyed")
-NSK_DIRECT = 1
+               "kg_submit_pages_keyed", "kg_dispatch_threshold", "kg_nsk_calibration")
+NSK_DIRECT, NSK_NOCAL = 1, 2
 HOST_STAGED, HOST_ZEROCOPY, HOST_AUTO = 0, 1, 2
 
 if not os.path.exists(LIB_PATH):
@@ -68,6 +68,17 @@ _lib.kg_alloc_pinned.argtypes = [ctypes.c_uint64]
 _lib.kg_alloc_pinned.restype = ctypes.c_void_p
 _lib.kg_free_pinned.argtypes = [ctypes.c_void_p]
 _lib.kg_free_pinned.restype = ctypes.c_int
+
+
+class CalibPoint(ctypes.Structure):
+    """kg_calib_point (include/kg.h)."""
+    _fields_ = [("bytes", ctypes.c_uint64), ("nsk_us", ctypes.c_double), ("launch_us", ctypes.c_double)]
+
+
+_lib.kg_dispatch_threshold.argtypes = [ctypes.POINTER(CalibPoint), ctypes.c_int]
+_lib.kg_dispatch_threshold.restype = ctypes.c_uint64
+_lib.kg_nsk_calibration.argtypes = [ctypes.POINTER(CalibPoint), ctypes.c_int]
+_lib.kg_nsk_calibration.restype = ctypes.c_int
 _lib.kg_launch_count.argtypes = []
 _lib.kg_launch_count.restype = ctypes.c_uint64
 
@@ -184,6 +195,19 @@ def nsk_dispatch(max_bytes: int = 0) -> int:
     out = ctypes.c_uint64(0)
     _check(_lib.kg_nsk_dispatch(int(max_bytes), ctypes.byref(out)), "kg_nsk_dispatch")
     return int(out.value)
+
+
+def dispatch_threshold(points) -> int:
+    """kg_dispatch_threshold over [(bytes, nsk_us, launch_us), ...]."""
+    arr = (CalibPoint * max(1, len(points)))(*[CalibPoint(int(b), float(n), float(l)) for b, n, l in points])
+    return int(_lib.kg_dispatch_threshold(arr, len(points)))
+
+
+def nsk_calibration():
+    """The last calibration's samples [(bytes, nsk_us, launch_us), ...]."""
+    arr = (CalibPoint * 16)()
+    n = _check(_lib.kg_nsk_calibration(arr, 16), "kg_nsk_calibration")
+    return [(int(p.bytes), float(p.nsk_us), float(p.launch_us)) for p in arr[:min(n, 16)]]
 
 
 def alloc_pinned(nbytes: int):

@@ -36,6 +36,9 @@ struct LaunchArgs {
     // tex_off + i.  0 = plain global loads.
     unsigned long long tex_in = 0;
     int64_t tex_off = 0;
+    // 1: in/out/ivs are reached over the host link (zero-copy): small batches
+    // then use fewer, larger CTAs (every CTA's first loads pay a link round trip)
+    uint32_t host_io = 0;
 };
 
 // Base (unreplicated) lookup tables, built on the host by the GPU-path code

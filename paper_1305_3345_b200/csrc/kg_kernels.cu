@@ -55,7 +55,17 @@ constexpr int kSmemDec = 2 * kRegion + 255 * 256 + 128;     // Td0..Td3 + Si (t 
 
 __device__ BaseTables g_tables;
 #ifdef KG_CTA_STAMPS
-__device__ unsigned long long g_stamps[148 * 34];
+// diagnostics build (tools/cta_stamps.cu): %globaltimer per CTA of the last 8
+// launches: [0] start, [1] tables filled, [2] griddepcontrol.wait returned,
+// [3 + w] warp w done (<= 32 warps)
+constexpr int kStampW = 36;
+__device__ unsigned long long g_stamps[8][148][kStampW];
+__device__ unsigned int g_stamp_ctr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #endif
 
 __device__ __forceinline__ uint32_t rotl32(uint32_t v, int s) { return __funnelshift_l(v, v, s); }
@@ -214,6 +224,24 @@ __device__ __forceinline__ uint64_t part_start(uint64_t n, uint64_t g, uint64_t 
     return k * q + (k < r ? k : r);
 }
 
+// A warp's contiguous share [w0, w1) of the CTA range [c0, c1) (units of one
+// lane item: a block or a block group).  Small ranges (at most one 32-item
+// unit per warp) go out in whole units, so every active warp runs all 32
+// lanes: a balanced split of, say, one 4 KiB page's 128 block pairs over 16
+// warps would leave 24 of 32 lanes idle in every lookup wavefront (4x the
+// LSU time of a small launch, profiles/r2_latency).  Larger ranges are split
+// evenly.
+__device__ __forceinline__ void small_split(uint64_t c0, uint64_t c1, uint32_t warp, uint32_t nwarps, uint64_t &w0,
+                                            uint64_t &w1) {
+    if (c1 - c0 <= 32ull * nwarps) {
+        w0 = c0 + 32ull * warp < c1 ? c0 + 32ull * warp : c1;
+        w1 = w0 + 32 < c1 ? w0 + 32 : c1;
+    } else {
+        w0 = c0 + part_start(c1 - c0, nwarps, warp);
+        w1 = c0 + part_start(c1 - c0, nwarps, warp + 1);
+    }
+}
+
 // Programmatic dependent launch (sm_90+): the table fill above does not touch
 // the batch, so it may overlap the tail of the previous kernel on the stream;
 // griddepcontrol.wait then blocks until that kernel has completed and its
@@ -299,8 +327,8 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
         c0 = part_start(nb, ncta, cta);
         c1 = part_start(nb, ncta, cta + 1);
     }
-    const uint64_t w0 = c0 + part_start(c1 - c0, nwarps, warp);
-    const uint64_t w1 = c0 + part_start(c1 - c0, nwarps, warp + 1);
+    uint64_t w0, w1;
+    small_split(c0, c1, warp, nwarps, w0, w1);
 
     // Per-lane position of block g = w0 + lane: page and index j in page.
     uint64_t page = (w0 + lane) / m;
@@ -440,8 +468,8 @@ __device__ __forceinline__ void blockgroup_body(const Job &a, const Cipher &cph,
         c1 = part_start(ng, ncta, cta + 1);
         cmid = c1;
     }
-    const uint64_t w0 = c0 + part_start(cmid - c0, nwarps, warp);
-    const uint64_t w1 = c0 + part_start(cmid - c0, nwarps, warp + 1);
+    uint64_t w0, w1;
+    small_split(c0, cmid, warp, nwarps, w0, w1);
     uint64_t page = (w0 + lane) / mg;
     uint32_t jg = (uint32_t)((w0 + lane) - page * mg);  // group index in the page
 
@@ -550,14 +578,18 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
     constexpr bool DEC = (DIR == 1);
     constexpr bool CBC = (MODE == 0);
 #ifdef KG_CTA_STAMPS
-    unsigned long long t_start;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    const unsigned long long t_start = gtimer();
+    __shared__ unsigned stamp_slot;
+    if (threadIdx.x == 0) stamp_slot = (atomicAdd(&g_stamp_ctr, 1u) / gridDim.x) & 7u;
 #endif
     fill_tables<DEC>(sm);
+#ifdef KG_CTA_STAMPS
+    __syncthreads();
+    const unsigned long long t_filled = gtimer();
+#endif
     pdl_prologue_done();
 #ifdef KG_CTA_STAMPS
-    unsigned long long t_filled;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_filled));
+    const unsigned long long t_waited = gtimer();
 #endif
     const uint32_t lb = lane_bytes();
     if (PAIR) {
@@ -568,13 +600,13 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
         else blockpar_body<false, CBC>(job_of(a), ParamEnc<NR>{sm, lb, a.rk}, blockIdx.x, gridDim.x);
     }
 #ifdef KG_CTA_STAMPS
-    // per-warp finish time; per-CTA start / tables-filled times (diagnostics build only)
-    unsigned long long t_end;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    if ((threadIdx.x & 31) == 0) g_stamps[blockIdx.x * 34 + 2 + (threadIdx.x >> 5)] = t_end;
+    const unsigned long long t_end = gtimer();
+    unsigned long long *st = g_stamps[stamp_slot][blockIdx.x];
+    if ((threadIdx.x & 31) == 0) st[3 + (threadIdx.x >> 5)] = t_end;
     if (threadIdx.x == 0) {
-        g_stamps[blockIdx.x * 34 + 0] = t_start;
-        g_stamps[blockIdx.x * 34 + 1] = t_filled;
+        st[0] = t_start;
+        st[1] = t_filled;
+        st[2] = t_waited;
     }
 #endif
 }
@@ -588,24 +620,29 @@ template <int NR, bool WIDE, bool TEX = false>
 __global__ void __launch_bounds__(kChainThreads, 1) kg_cbc_enc(const __grid_constant__ LaunchArgs a) {
     extern __shared__ __align__(16) char sm[];
 #ifdef KG_CTA_STAMPS
-    unsigned long long t_start;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    const unsigned long long t_start = gtimer();
+    __shared__ unsigned stamp_slot;
+    if (threadIdx.x == 0) stamp_slot = (atomicAdd(&g_stamp_ctr, 1u) / gridDim.x) & 7u;
 #endif
     fill_tables<false>(sm);
+#ifdef KG_CTA_STAMPS
+    __syncthreads();
+    const unsigned long long t_filled = gtimer();
+#endif
     pdl_prologue_done();
     __syncthreads();
 #ifdef KG_CTA_STAMPS
-    unsigned long long t_filled;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_filled));
+    const unsigned long long t_waited = gtimer();
 #endif
     cbc_enc_body<WIDE, ParamEnc<NR>, TEX>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
 #ifdef KG_CTA_STAMPS
-    unsigned long long t_end;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    if ((threadIdx.x & 31) == 0) g_stamps[blockIdx.x * 34 + 2 + (threadIdx.x >> 5)] = t_end;
+    const unsigned long long t_end = gtimer();
+    unsigned long long *st = g_stamps[stamp_slot][blockIdx.x];
+    if ((threadIdx.x & 31) == 0) st[3 + (threadIdx.x >> 5)] = t_end;
     if (threadIdx.x == 0) {
-        g_stamps[blockIdx.x * 34 + 0] = t_start;
-        g_stamps[blockIdx.x * 34 + 1] = t_filled;
+        st[0] = t_start;
+        st[1] = t_filled;
+        st[2] = t_waited;
     }
 #endif
 }
@@ -939,7 +976,10 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
         if (wide) return launch_pdl_tpb(kg_cbc_enc<NR, true>, grid, kChainThreads, kSmemEnc, st, a);
         return launch_pdl_tpb(kg_cbc_enc<NR, false>, grid, kChainThreads, kSmemEnc, st, a);
     }
-    uint64_t want = (nb + 255) / 256;
+    // one CTA per 64 blocks (one warp unit of block pairs) up to one per SM:
+    // small batches spread over many SMs, each filling its tables in parallel
+    // (zero-copy batches: one per 256 blocks, profiles/r2_latency)
+    uint64_t want = a.host_io ? (nb + 255) / 256 : (nb + 63) / 64;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
     if (want < 1) want = 1;
@@ -979,7 +1019,7 @@ template <int NR>
 cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedArgs &k, int num_sms, cudaStream_t st) {
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     const bool chain = (dir == 0 && mode == 0);
-    uint64_t want = chain ? a.n_pages : (nb + 255) / 256;
+    uint64_t want = chain ? a.n_pages : a.host_io ? (nb + 255) / 256 : (nb + 63) / 64;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
     if (want < 1) want = 1;

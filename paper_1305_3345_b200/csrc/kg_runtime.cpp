@@ -29,6 +29,7 @@
 #include <sys/mman.h>
 #include <time.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <thread>
@@ -69,6 +70,8 @@ struct Nsk {
     uint64_t gen = 0;            // incremented at every stop
     uint64_t dispatch_bytes = UINT64_MAX;  // requests up to this size go to the NSK (row f2)
     uint8_t *cal_in = nullptr, *cal_out = nullptr, *cal_iv = nullptr;  // calibration scratch
+    kg_calib_point cal[16];      // the last calibration's curves (row f2)
+    int n_cal = 0;
 };
 
 typedef CUresult (*PFN_writeValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
@@ -1088,6 +1091,7 @@ int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n
                             (g.host_path == KG_HOST_AUTO && !chain && total <= g.zc_max_bytes));
     if (all_device || zero_copy) {
         kg::LaunchArgs a;
+        a.host_io = all_device ? 0 : 1;
         a.in = reinterpret_cast<const uint4 *>(zin);
         a.out = reinterpret_cast<uint4 *>(const_cast<void *>(zout));
         a.ivs = need_iv ? reinterpret_cast<const uint4 *>(ziv) : nullptr;
@@ -1235,6 +1239,7 @@ int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint
     a.n_pages = n_pages;
     a.m = page_bytes / 16;
     a.in_place = (in == out);
+    a.host_io = (all_device || staged) ? 0 : 1;
     kg::KeyedArgs k;
     k.key_ids = reinterpret_cast<const uint16_t *>(zid);
     k.tab = tab;
@@ -1372,11 +1377,14 @@ int kg_poll(int64_t ticket) {
     return cuda_fail(e, "cudaEventQuery");
 }
 
+int nsk_cal_alloc();
+int nsk_calibrate(uint64_t *chosen);
+
 int kg_nsk_start(int ctas, int flags, uint32_t idle_ms) {
     std::lock_guard<std::mutex> lk(g_mu);
     DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
-    if (flags & ~KG_NSK_DIRECT) return KG_EINVAL;
+    if (flags & ~(KG_NSK_DIRECT | KG_NSK_NOCAL)) return KG_EINVAL;
     if (ctas == 0) ctas = 16;
     if (ctas < 0 || ctas > g.num_sms) return KG_EINVAL;
     if (g.nsk.on) return KG_EINVAL;
@@ -1400,10 +1408,23 @@ int kg_nsk_start(int ctas, int flags, uint32_t idle_ms) {
     KG_CU(cudaStreamCreateWithFlags(&n.st, cudaStreamNonBlocking));
     g.nsk = n;
     g.nsk.on = true;
-    int rc = nsk_launch(1);
+    int rc = (flags & KG_NSK_NOCAL) ? KG_OK : nsk_cal_alloc();
+    if (rc == KG_OK) rc = nsk_launch(1);
+    // "calibrate it using microbenchmarks at boot time"
+    if (rc == KG_OK && !(flags & KG_NSK_NOCAL)) {
+        rc = nsk_calibrate(nullptr);
+        if (rc != KG_OK) {
+            nsk_stop_locked();
+            return rc;
+        }
+        return KG_OK;
+    }
     if (rc != KG_OK) {
         cudaFreeHost(g.nsk.ring);
         cudaFree(g.nsk.ctl);
+        cudaFree(g.nsk.cal_in);
+        cudaFree(g.nsk.cal_out);
+        cudaFree(g.nsk.cal_iv);
         cudaStreamDestroy(g.nsk.st);
         const uint64_t gen = g.nsk.gen;
         g.nsk = Nsk();
@@ -1422,19 +1443,32 @@ static double now_s() {
     return t.tv_sec + 1e-9 * t.tv_nsec;
 }
 
-int nsk_calibrate(uint64_t *chosen) {
-    const uint32_t pb = 4096;
-    const uint64_t max_pages = 1u << 13;  // up to 32 MiB
-    // Scratch lives until kg_nsk_stop: cudaFree would synchronise the whole
-    // device, i.e. wait for the resident kernel's idle exit.
-    if (!g.nsk.cal_in) {
-        if (cudaMalloc(&g.nsk.cal_in, max_pages * pb) != cudaSuccess ||
-            cudaMalloc(&g.nsk.cal_out, max_pages * pb) != cudaSuccess ||
-            cudaMalloc(&g.nsk.cal_iv, max_pages * 16) != cudaSuccess) {
-            cudaGetLastError();
-            return KG_ENOMEM;
-        }
+// Scratch for the calibration, allocated before the NSK is launched (cudaMalloc
+// / cudaFree may synchronise the device, i.e. wait for the resident kernel).
+constexpr uint64_t kCalMaxPages = 1u << 13;  // calibration sizes 4 KiB .. 32 MiB
+constexpr uint32_t kCalPageBytes = 4096;
+
+int nsk_cal_alloc() {
+    if (g.nsk.cal_in) return KG_OK;
+    if (cudaMalloc(&g.nsk.cal_in, kCalMaxPages * kCalPageBytes) != cudaSuccess ||
+        cudaMalloc(&g.nsk.cal_out, kCalMaxPages * kCalPageBytes) != cudaSuccess ||
+        cudaMalloc(&g.nsk.cal_iv, kCalMaxPages * 16) != cudaSuccess) {
+        cudaGetLastError();
+        return KG_ENOMEM;
     }
+    KG_CU(cudaMemset(g.nsk.cal_in, 0x5a, kCalMaxPages * kCalPageBytes));
+    KG_CU(cudaMemset(g.nsk.cal_iv, 0x33, kCalMaxPages * 16));
+    return KG_OK;
+}
+
+// The paper's "calibrate it using microbenchmarks at boot time": time both
+// GPU paths, caller-observed (post + spin on the completion word vs launch +
+// stream synchronise), on AES-128-CBC decrypt batches of 1, 2, 4, ... pages
+// (device memory, median of 5 after 2 warm-ups), stopping two sizes after
+// the launch first wins; the threshold follows kg_dispatch_threshold.
+int nsk_calibrate(uint64_t *chosen) {
+    int rc = nsk_cal_alloc();
+    if (rc != KG_OK) return rc;
     uint8_t *d_in = g.nsk.cal_in, *d_out = g.nsk.cal_out, *d_iv = g.nsk.cal_iv;
     uint8_t key[16];
     for (int i = 0; i < 16; i++) key[i] = (uint8_t)(17 * i + 1);
@@ -1442,46 +1476,47 @@ int nsk_calibrate(uint64_t *chosen) {
     const int nr = kg::expand_key(key, 16, &enc, &dec);
     cudaStream_t st;
     KG_CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    cudaMemsetAsync(d_in, 0x5a, max_pages * pb, st);
-    cudaMemsetAsync(d_iv, 0x33, max_pages * 16, st);
-    cudaStreamSynchronize(st);
-    uint64_t best = 0;
-    int rc = KG_OK;
-    for (uint64_t pages = 1; pages <= max_pages && rc == KG_OK; pages *= 4) {
-        double t_nsk = 1e9, t_launch = 1e9;
-        for (int rep = 0; rep < 7; rep++) {
-            double t0 = now_s();
-            const int64_t seq = nsk_post(1, d_in, d_out, d_iv, pages, pb / 16, 0, nr, &dec, st, true);
+    g.nsk.n_cal = 0;
+    int launch_wins = 0;
+    for (uint64_t pages = 1; pages <= kCalMaxPages && rc == KG_OK && launch_wins < 2; pages *= 2) {
+        double tn[7], tl[7];
+        for (int rep = 0; rep < 7 && rc == KG_OK; rep++) {
+            const double t0 = now_s();
+            const int64_t seq = nsk_post(1, d_in, d_out, d_iv, pages, kCalPageBytes / 16, 0, nr, &dec, st, true);
             if (seq < 0) {
                 rc = (int)seq;
                 break;
             }
             const uint64_t *done = &g.nsk.ring->done[(seq - 1) % kg::kNskSlots];
             while (vload(done) < (uint64_t)seq) cpu_relax();
-            double t1 = now_s();
+            const double t1 = now_s();
             kg::LaunchArgs a;
             a.in = reinterpret_cast<const uint4 *>(d_in);
             a.out = reinterpret_cast<uint4 *>(d_out);
             a.ivs = reinterpret_cast<const uint4 *>(d_iv);
             a.n_pages = pages;
-            a.m = pb / 16;
+            a.m = kCalPageBytes / 16;
             a.in_place = 0;
             a.rk = dec;
             rc = launch(1, 0, nr, a, st);
             if (rc != KG_OK) break;
-            cudaStreamSynchronize(st);
-            double t2 = now_s();
-            if (rep >= 2) {  // first reps warm up
-                t_nsk = (t1 - t0) < t_nsk ? (t1 - t0) : t_nsk;
-                t_launch = (t2 - t1) < t_launch ? (t2 - t1) : t_launch;
-            }
+            if (cudaStreamSynchronize(st) != cudaSuccess) rc = KG_ECUDA;
+            tn[rep] = t1 - t0;
+            tl[rep] = now_s() - t1;
         }
-        if (t_nsk <= t_launch) best = pages * pb;  // a tie goes to the resident kernel
+        if (rc != KG_OK) break;
+        std::sort(tn + 2, tn + 7);
+        std::sort(tl + 2, tl + 7);
+        kg_calib_point &pt = g.nsk.cal[g.nsk.n_cal++];
+        pt.bytes = pages * kCalPageBytes;
+        pt.nsk_us = 1e6 * tn[4];
+        pt.launch_us = 1e6 * tl[4];
+        if (pt.launch_us < pt.nsk_us) launch_wins++;
     }
     cudaStreamDestroy(st);
     if (rc != KG_OK) return rc;
-    g.nsk.dispatch_bytes = best;
-    if (chosen) *chosen = best;
+    g.nsk.dispatch_bytes = kg_dispatch_threshold(g.nsk.cal, g.nsk.n_cal);
+    if (chosen) *chosen = g.nsk.dispatch_bytes;
     return KG_OK;
 }
 
@@ -1494,6 +1529,23 @@ int kg_nsk_dispatch(uint64_t max_bytes, uint64_t *chosen) {
     g.nsk.dispatch_bytes = max_bytes;
     if (chosen) *chosen = max_bytes;
     return KG_OK;
+}
+
+uint64_t kg_dispatch_threshold(const kg_calib_point *pts, int n) {
+    if (!pts || n <= 0) return UINT64_MAX;
+    for (int i = 0; i < n; i++)
+        if (pts[i].launch_us < pts[i].nsk_us)  // a tie goes to the resident kernel
+            return i == 0 ? 0 : pts[i - 1].bytes;
+    return UINT64_MAX;
+}
+
+int kg_nsk_calibration(kg_calib_point *pts, int max_pts) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g.up) return KG_ENOTINIT;
+    if (max_pts < 0 || (max_pts > 0 && !pts)) return KG_EINVAL;
+    const int n = g.nsk.n_cal < max_pts ? g.nsk.n_cal : max_pts;
+    for (int i = 0; i < n; i++) pts[i] = g.nsk.cal[i];
+    return g.nsk.n_cal;
 }
 
 int kg_nsk_stop(void) {

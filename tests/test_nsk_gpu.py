@@ -37,7 +37,7 @@ def run(kg, torch, direction, mode, key, data, n, pb, ivs, where, inplace=False,
 @pytest.mark.parametrize("where", ["device", "pinned"])
 def test_nsk_parity(nsk, flags, where):
     kg, torch = nsk
-    kg.nsk_start(8, flags, 5000)
+    kg.nsk_start(8, flags | kg.NSK_NOCAL, 5000)
     for (n, pb, kb) in [(1, 4096, 16), (16, 4096, 32), (33, 512, 24), (300, 4096, 16), (5, 16, 32), (1000, 48, 16)]:
         key = synth.make_key(kb, seed=n + pb)
         data = synth.make_pages(n, pb, seed=n * 7 + pb)
@@ -53,7 +53,7 @@ def test_nsk_parity(nsk, flags, where):
 
 def test_nsk_ring_wraparound_and_many_inflight(nsk):
     kg, torch = nsk
-    kg.nsk_start(4, kg.NSK_DIRECT, 5000)
+    kg.nsk_start(4, kg.NSK_DIRECT | kg.NSK_NOCAL, 5000)
     n, pb = 4, 4096
     key = synth.make_key(16, seed=1)
     kg.set_key(0, key)
@@ -73,7 +73,7 @@ def test_nsk_ring_wraparound_and_many_inflight(nsk):
 
 def test_nsk_idle_exit_and_relaunch(nsk):
     kg, torch = nsk
-    kg.nsk_start(2, kg.NSK_DIRECT, 30)        # 30 ms idle watchdog
+    kg.nsk_start(2, kg.NSK_DIRECT | kg.NSK_NOCAL, 30)        # 30 ms idle watchdog
     key = synth.make_key(16, seed=9)
     data = synth.make_pages(8, 4096, seed=10)
     ivs = synth.make_ivs(8, seed=11)
@@ -101,7 +101,7 @@ y = torch.empty_like(x)
 ref = torch.empty_like(x)
 kg.wait(kg.submit_pages(1, 0, x, ref, 1, 4096, iv, 0))
 torch.cuda.synchronize()
-kg.nsk_start(2, flags, 1)                 # 1 ms idle watchdog
+kg.nsk_start(2, flags | kg.NSK_NOCAL, 1)                 # 1 ms idle watchdog
 rnd = random.Random(11)
 l0 = kg.launch_count()
 for i in range(600):
@@ -136,7 +136,7 @@ def test_nsk_stream_ordering(nsk):
     """Ordered mode: the doorbell is rung by the stream after earlier work,
     and later work on the stream sees the result."""
     kg, torch = nsk
-    kg.nsk_start(8, 0, 5000)
+    kg.nsk_start(8, kg.NSK_NOCAL, 5000)
     n, pb = 2048, 4096
     key = synth.make_key(16, seed=20)
     kg.set_key(0, key)
@@ -161,7 +161,7 @@ def test_nsk_stream_ordering(nsk):
 
 def test_nsk_stop_with_outstanding_and_restart(nsk):
     kg, torch = nsk
-    kg.nsk_start(4, kg.NSK_DIRECT, 5000)
+    kg.nsk_start(4, kg.NSK_DIRECT | kg.NSK_NOCAL, 5000)
     n, pb = 64, 4096
     kg.set_key(0, synth.make_key(16, seed=30))
     x = torch.from_numpy(synth.make_pages(n, pb, seed=31)).cuda()
@@ -175,7 +175,7 @@ def test_nsk_stop_with_outstanding_and_restart(nsk):
     assert lib.kg_nsk_stop() == kg.OK          # idempotent
     assert lib.kg_nsk_start(10 ** 6, 0, 0) == kg.EINVAL
     assert lib.kg_nsk_start(2, 8, 0) == kg.EINVAL
-    kg.nsk_start(2, 0, 0)
+    kg.nsk_start(2, kg.NSK_NOCAL, 0)
     assert lib.kg_nsk_start(2, 0, 0) == kg.EINVAL   # already running
     ref = torch.empty_like(x)
     kg.wait(kg.submit_pages(0, 0, x, ref, n, pb, iv, 0))
@@ -216,7 +216,7 @@ def test_nsk_multithreaded_soak(nsk):
     outputs are right."""
     import threading
     kg, torch = nsk
-    kg.nsk_start(8, kg.NSK_DIRECT, 5000)
+    kg.nsk_start(8, kg.NSK_DIRECT | kg.NSK_NOCAL, 5000)
     n, pb = 16, 4096
     key = synth.make_key(16, seed=77)
     kg.set_key(3, key)
@@ -258,7 +258,7 @@ def test_keyed_batches_while_nsk_runs(nsk, where):
     """Mixed-key batches are launched on the SMs the NSK leaves free (a grid
     over all SMs would wait behind the resident NSK forever)."""
     kg, torch = nsk
-    kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+    kg.nsk_start(16, kg.NSK_DIRECT | kg.NSK_NOCAL, 5000)
     keys = {kid: synth.make_key(16, seed=300 + kid) for kid in (5, 6, 7)}
     for kid, k in keys.items():
         kg.set_key(kid, k)
@@ -281,3 +281,36 @@ def test_keyed_batches_while_nsk_runs(nsk, where):
         kg.wait(kg.submit_pages_keyed(d, mode, tin, tout, n, 4096, tiv, tid, 16, s))
         s.synchronize()
         assert first_mismatch(tout.cpu().numpy(), exp) is None, (d, mode, n)
+
+
+def test_nsk_start_calibrates_and_dispatch_is_monotone(nsk):
+    """Row f2 as built: kg_nsk_start calibrates the NSK/launch crossover at
+    start (the paper's "calibrate it using microbenchmarks at boot time",
+    PAPER.md:493-495); the threshold is kg_dispatch_threshold of the recorded
+    samples, and the dispatch it implies is monotone: every request up to it
+    goes to the NSK (no launch), every larger one is launched."""
+    kg, torch = nsk
+    kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+    pts = kg.nsk_calibration()
+    assert len(pts) >= 2 and [p[0] for p in pts] == [4096 << i for i in range(len(pts))]
+    assert all(p[1] > 0 and p[2] > 0 for p in pts)
+    chosen = kg.dispatch_threshold(pts)
+    key = synth.make_key(16, seed=60)
+    kg.set_key(0, key)
+    nmax = 1 << 13
+    x = torch.from_numpy(synth.make_pages(nmax, 4096, seed=61)).cuda()
+    iv = torch.from_numpy(synth.make_ivs(nmax, seed=62)).cuda()
+    y = torch.empty_like(x)
+    s = torch.cuda.current_stream()
+    s.synchronize()
+    routed = []
+    for k in range(14):
+        n = 1 << k
+        l0 = kg.launch_count()
+        kg.wait(kg.submit_pages(1, 0, x, y, n, 4096, iv, 0))
+        routed.append(kg.launch_count() - l0 == 0)          # True: served by the NSK
+        assert routed[-1] == (n * 4096 <= chosen), (n, chosen, pts)
+    assert routed == sorted(routed, reverse=True)           # monotone
+    s.synchronize()
+    exp = oracle_pages(1, 0, key, x.cpu().numpy(), nmax, 4096, iv.cpu().numpy())
+    assert first_mismatch(y.cpu().numpy(), exp) is None

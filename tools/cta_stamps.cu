@@ -1,14 +1,24 @@
-// cta_stamps.cu -- diagnostics: per-CTA start / tables-filled and per-warp
-// finish times (%globaltimer) of one C2 decrypt launch, to see where the
-// per-launch overhead goes (launch ramp, table fill, tail).  Builds the
-// kernels with -DKG_CTA_STAMPS by including their source.
+// cta_stamps.cu -- diagnostics: where the per-launch overhead of back-to-back
+// launches goes.  Builds the kernels with -DKG_CTA_STAMPS (per-CTA %globaltimer
+// at start, tables filled, griddepcontrol.wait returned, per-warp done; last 8
+// launches) by including their source, runs 12 back-to-back C2 decrypt (or C3
+// encrypt: argv[1] = "enc") launches exactly as kg_submit_pages does (PDL), and
+// prints, for launches 8..11 of the run, the per-CTA rows plus a summary:
+//   ramp   = last CTA start - first CTA start
+//   fill   = median (filled - start)
+//   gap    = first wait-release of launch k - last warp done of launch k-1
+//   spread = last warp done - first warp done (the tail)
+//   period = first wait-release of launch k+1 - first wait-release of launch k
 #define KG_CTA_STAMPS 1
 #include "../paper_1305_3345_b200/csrc/kg_kernels.cu"
 
 #include <stdio.h>
 
+#include <algorithm>
+#include <vector>
+
 int main(int argc, char **argv) {
-    const bool enc = argc > 1 && argv[1][0] == 'e';  // "enc": C3 AES-256-CBC encrypt 1 GiB
+    const bool enc = argc > 1 && argv[1][0] == 'e';
     kg::BaseTables t;
     kg::build_base_tables(&t);
     if (kg::kernels_init(t) != cudaSuccess) return 1;
@@ -29,22 +39,65 @@ int main(int argc, char **argv) {
     a.m = pb / 16;
     a.in_place = 0;
     a.rk = enc ? enc_k : dec_k;
-    for (int rep = 0; rep < 5; rep++) kg::launch_pages(enc ? 0 : 1, 0, enc ? 14 : 10, a, 148, 0);
-    cudaDeviceSynchronize();
-    static unsigned long long h[148 * 34];
+    // the texture-pipe input the runtime uses for device batches
+    cudaResourceDesc rd = {};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = in;
+    rd.res.linear.desc = cudaCreateChannelDesc<uint4>();
+    rd.res.linear.sizeInBytes = n * pb;
+    cudaTextureDesc td = {};
+    td.readMode = cudaReadModeElementType;
+    cudaTextureObject_t tex = 0;
+    if (cudaCreateTextureObject(&tex, &rd, &td, nullptr) == cudaSuccess) a.tex_in = tex;
+    const unsigned zero = 0;
+    cudaMemcpyToSymbol(kg::g_stamp_ctr, &zero, 4);
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    for (int rep = 0; rep < 12; rep++) kg::launch_pages(enc ? 0 : 1, 0, enc ? 14 : 10, a, 148, st);
+    cudaStreamSynchronize(st);
+    static unsigned long long h[8][148][kg::kStampW];
     cudaMemcpyFromSymbol(h, kg::g_stamps, sizeof h);
+    const int warps = enc ? 32 : 16;
+    // launches 4..11 live in slots 4..7, 0..3
+    std::vector<int> order = {4, 5, 6, 7, 0, 1, 2, 3};
     unsigned long long t0 = ~0ull;
-    for (int c = 0; c < 148; c++) t0 = h[c * 34] < t0 ? h[c * 34] : t0;
-    printf("{\"cta\": [");
-    for (int c = 0; c < 148; c++) {
-        unsigned long long wmin = ~0ull, wmax = 0;
-        for (int w = 0; w < 32; w++) {
-            unsigned long long v = h[c * 34 + 2 + w];
-            wmin = v < wmin ? v : wmin;
-            wmax = v > wmax ? v : wmax;
+    for (int c = 0; c < 148; c++) t0 = std::min(t0, h[order[0]][c][0]);
+    double prev_last_done = -1, prev_first_wait = -1;
+    printf("{\"launches\": [");
+    for (size_t k = 0; k < order.size(); k++) {
+        auto &L = h[order[k]];
+        std::vector<double> start, fill, wait, done_first, done_last;
+        for (int c = 0; c < 148; c++) {
+            start.push_back((L[c][0] - t0) * 1e-3);
+            fill.push_back((L[c][1] - L[c][0]) * 1e-3);
+            wait.push_back((L[c][2] - t0) * 1e-3);
+            double dmin = 1e30, dmax = 0;
+            for (int w = 0; w < warps; w++) {
+                const double d = (L[c][3 + w] - t0) * 1e-3;
+                dmin = std::min(dmin, d);
+                dmax = std::max(dmax, d);
+            }
+            done_first.push_back(dmin);
+            done_last.push_back(dmax);
         }
-        printf("%s[%llu, %llu, %llu, %llu]", c ? ", " : "", h[c * 34] - t0, h[c * 34 + 1] - t0, wmin - t0, wmax - t0);
+        auto mn = [](std::vector<double> v) { return *std::min_element(v.begin(), v.end()); };
+        auto mx = [](std::vector<double> v) { return *std::max_element(v.begin(), v.end()); };
+        auto med = [](std::vector<double> v) {
+            std::sort(v.begin(), v.end());
+            return v[v.size() / 2];
+        };
+        const double first_wait = mn(wait), last_done = mx(done_last);
+        printf("%s{\"k\": %zu, \"first_start_us\": %.2f, \"ramp_us\": %.2f, \"fill_us_median\": %.2f, \"fill_us_max\": %.2f, "
+               "\"first_wait_us\": %.2f, \"last_wait_us\": %.2f, \"gap_after_prev_done_us\": %.2f, "
+               "\"first_done_us\": %.2f, \"last_done_us\": %.2f, \"tail_spread_us\": %.2f, \"period_us\": %.2f}",
+               k ? ", " : "", k, mn(start), mx(start) - mn(start), med(fill), mx(fill), first_wait, mx(wait),
+               prev_last_done >= 0 ? first_wait - prev_last_done : -1.0, mn(done_first), last_done,
+               last_done - mn(done_last), prev_first_wait >= 0 ? first_wait - prev_first_wait : -1.0);
+        prev_last_done = last_done;
+        prev_first_wait = first_wait;
     }
     printf("]}\n");
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e));
     return 0;
 }

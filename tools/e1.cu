@@ -54,6 +54,20 @@ __global__ void empty_kernel(const uint4 *in, uint4 *sink) {
     if (threadIdx.x == 0x7fffffff) sink[0] = in[0];
 }
 
+__global__ void empty_smem_kernel(const uint4 *in, uint4 *sink) {
+    extern __shared__ uint4 smem[];
+    if (threadIdx.x == 0x7fffffff) sink[0] = smem[in[0].x];
+}
+
+// writes 192 KB of shared memory with conflict-free 32-bit stores (the page
+// kernels' table-fill traffic, without its global loads)
+__global__ void fill_smem_kernel(const uint4 *in, uint4 *sink) {
+    extern __shared__ uint32_t sw[];
+    for (int i = threadIdx.x; i < 196480 / 4; i += blockDim.x) sw[i] = i;
+    __syncthreads();
+    if (threadIdx.x == 0x7fffffff) sink[0].x = sw[in[0].x];
+}
+
 struct Mailbox {                 // mapped pinned memory
     volatile uint64_t doorbell;  // host -> GPU: request seq
     uint64_t pad0[7];
@@ -189,6 +203,33 @@ int main(int argc, char **argv) {
         CK(cudaFree(arrive));
         CK(cudaFree(go));
         CK(cudaFreeHost(mb));
+    }
+
+    // ---- launch-latency pieces (no H2D): an empty kernel as is, with the
+    // 192 KB dynamic shared memory the page kernels reserve, and with a
+    // 192 KB allocation it also fills like the page kernels' table fill
+    {
+        const int big = 196480;
+        CK(cudaFuncSetAttribute(empty_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+        CK(cudaFuncSetAttribute(fill_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+        struct Arm {
+            const char *name;
+            int which;
+        } arms[] = {{"empty_512thr_sync", 0}, {"empty_512thr_192KB_smem_sync", 1}, {"fill_192KB_smem_512thr_sync", 2}};
+        for (auto &arm : arms) {
+            for (int pass = 0; pass < 2; pass++) {
+                v.clear();
+                for (int i = 0; i < reps; i++) {
+                    const double t0 = now_us();
+                    if (arm.which == 0) empty_kernel<<<1, 512, 0, st>>>(d_in, d_sink);
+                    else if (arm.which == 1) empty_smem_kernel<<<1, 512, big, st>>>(d_in, d_sink);
+                    else fill_smem_kernel<<<1, 512, big, st>>>(d_in, d_sink);
+                    cudaStreamSynchronize(st);
+                    v.push_back(now_us() - t0);
+                }
+            }
+            report(arm.name, 512, v);
+        }
     }
 
     // ---- host-side pieces of a submit (for the submit-path breakdown)

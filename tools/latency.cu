@@ -82,6 +82,18 @@ int main(int argc, char **argv) {
             }
         }
         report("kg_hbm_dec", v, pages);
+        // the same, completion by stream synchronisation instead of kg_wait
+        for (int pass = 0; pass < 2; pass++) {
+            v.clear();
+            for (int i = 0; i < reps; i++) {
+                double t0 = now_us();
+                int64_t t = kg_submit_pages(KG_DECRYPT, KG_MODE_CBC, d_in, d_out, pages, PB, d_iv, 0, st);
+                cudaStreamSynchronize(st);
+                v.push_back(now_us() - t0);
+                kg_wait(t);
+            }
+        }
+        report("kg_hbm_dec_streamsync", v, pages);
         for (int pass = 0; pass < 2; pass++) {
             v.clear();
             for (int i = 0; i < reps; i++) {
@@ -95,7 +107,7 @@ int main(int argc, char **argv) {
     }
     // the NSK (row f3): persistent service kernel, requests as messages in pinned memory
     for (int flags : {KG_NSK_DIRECT, 0}) {
-        if (kg_nsk_start(16, flags, 5000) != KG_OK) {
+        if (kg_nsk_start(16, flags | KG_NSK_NOCAL, 5000) != KG_OK) {
             printf("{\"error\": \"kg_nsk_start failed\"}\n");
             continue;
         }

@@ -46,7 +46,7 @@ for n, pb in [(3, 4096), (5, 48), (40, 512)]:
             x = data.clone()
             kg.wait(kg.submit_pages_keyed(d, mode, x, x, n, pb, ivs if mode == 0 else None, ids, 16))
             assert torch.equal(x, out)
-kg.nsk_start(2, kg.NSK_DIRECT, 2000)
+kg.nsk_start(2, kg.NSK_DIRECT | kg.NSK_NOCAL, 2000)
 n, pb = 4, 4096
 data = torch.from_numpy(synth.make_pages(n, pb)).cuda()
 ivs = torch.from_numpy(synth.make_ivs(n)).cuda()

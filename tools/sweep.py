@@ -80,7 +80,7 @@ def main():
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
         tn = tnp = None
         if n <= 4096:  # the NSK (row f3), direct doorbell, 16 SMs
-            kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+            kg.nsk_start(16, kg.NSK_DIRECT | kg.NSK_NOCAL, 5000)
             for _ in range(5):
                 run_hbm()
             tn = lat(run_hbm, reps)
