@@ -36,6 +36,9 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>       // header-only NVTX v3: no-ops unless a profiler is attached
+#include <nvtx3/nvToolsExtCudaRt.h>
+
 #include "../../include/kg.h"
 #include "kg_internal.h"
 
@@ -233,6 +236,25 @@ void trace_dump() {
     for (auto &t : g_trace) cudaEventDestroy(t.ev);
     g_trace.clear();
 }
+// NVTX ranges (domain "kgpu") around the API calls and each staged chunk's
+// enqueue, and names for the internal streams, for nsys / ncu --nvtx timelines
+// (SURVEY.md §5 "Tracing").  Without a tool attached each is a no-op call.
+nvtxDomainHandle_t nvtx_domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("kgpu");
+    return d;
+}
+struct NvtxRange {
+    explicit NvtxRange(const char *msg) {
+        nvtxEventAttributes_t a = {};
+        a.version = NVTX_VERSION;
+        a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        a.message.ascii = msg;
+        nvtxDomainRangePushEx(nvtx_domain(), &a);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+};
+
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_nsk_waiters{0};
 
@@ -602,6 +624,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         const uint64_t np = sched[i];
         const uint64_t off = p0 * page_bytes, nbytes = np * page_bytes;
         Slot &s = g.slots[i % (uint64_t)g.n_slots];
+        NvtxRange nv_chunk("kg staged chunk (H2D, kernel, D2H enqueue)");
         // H2D stage: wait until the slot's previous output has drained.
         KG_CU(cudaStreamWaitEvent(g.s_h2d, s.freed, 0));
         if (kin == K_HOST) KG_CU(cudaMemcpyAsync(s.data, in + off, nbytes, cudaMemcpyHostToDevice, g.s_h2d));
@@ -841,6 +864,9 @@ int kg_init(int device) {
     KG_CU(cudaStreamCreateWithFlags(&g.s_h2d, cudaStreamNonBlocking));
     KG_CU(cudaStreamCreateWithFlags(&g.s_comp, cudaStreamNonBlocking));
     KG_CU(cudaStreamCreateWithFlags(&g.s_d2h, cudaStreamNonBlocking));
+    nvtxNameCudaStreamA(g.s_h2d, "kgpu H2D");
+    nvtxNameCudaStreamA(g.s_comp, "kgpu compute");
+    nvtxNameCudaStreamA(g.s_d2h, "kgpu D2H");
     KG_CU(cudaEventCreateWithFlags(&g.ev_begin, cudaEventDisableTiming));
     for (int b = 0; b < 2; b++) KG_CU(cudaEventCreateWithFlags(&g.iv_free[b], cudaEventDisableTiming));
     for (int i = 0; i < kMaxSlots; i++) {
@@ -1038,6 +1064,7 @@ int kg_set_key(int key_id, const uint8_t *key, int key_bytes) {
 
 int64_t kg_submit_pages(int dir, int mode, const void *in, void *out, uint64_t n_pages, uint32_t page_bytes,
                         const void *ivs, int key_id, void *stream) {
+    NvtxRange nv("kg_submit_pages");
     std::lock_guard<std::mutex> lk(g_mu);
     DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
@@ -1182,6 +1209,7 @@ static int keyed_snapshot(cudaStream_t st, const kg::DevKeyTable **out) {
 
 int64_t kg_submit_pages_keyed(int dir, int mode, const void *in, void *out, uint64_t n_pages, uint32_t page_bytes,
                               const void *ivs, const uint16_t *key_ids, int key_bytes, void *stream) {
+    NvtxRange nv("kg_submit_pages_keyed");
     std::lock_guard<std::mutex> lk(g_mu);
     DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
@@ -1303,6 +1331,7 @@ int nsk_ticket_state(const Ticket &t) {
 }
 
 int kg_wait(int64_t ticket) {
+    NvtxRange nv("kg_wait");
     cudaEvent_t ev;
     Ticket nsk_ticket;
     const uint64_t *done_word = nullptr;
@@ -1381,6 +1410,7 @@ int nsk_cal_alloc();
 int nsk_calibrate(uint64_t *chosen);
 
 int kg_nsk_start(int ctas, int flags, uint32_t idle_ms) {
+    NvtxRange nv("kg_nsk_start");
     std::lock_guard<std::mutex> lk(g_mu);
     DeviceGuard dg;
     if (!g.up) return KG_ENOTINIT;
