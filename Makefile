@@ -43,8 +43,14 @@ build/kgpu_crypt: examples/kgpu_crypt.c include/kg.h $(LIB) | build
 	gcc -std=c99 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lkgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 # diagnostics (not part of `all`): copy-engine overlap, per-CTA stamps, bitsliced round
-tools: build/copy_overlap build/cta_stamps build/bitslice_bench build/soak_tsan build/pipes_tex build/pipes_lds build/pipes_ldpath \
+tools: build/zc_duplex build/bitslice_bp build/copy_overlap build/cta_stamps build/bitslice_bench build/soak_tsan build/pipes_tex build/pipes_lds build/pipes_ldpath \
        build/hybrid_bench build/pipe_variants
+
+build/zc_duplex: tools/zc_duplex.cu | build
+	$(NVCC) -O2 -std=c++17 $(ARCH) -o $@ $<
+
+build/bitslice_bp: tools/bitslice_bp.cu tools/kg_sbox_bp.cuh tools/kg_sbox_bs.cuh | build
+	$(NVCC) -O3 -std=c++17 $(ARCH) -Itools -o $@ $<
 
 build/copy_overlap: tools/copy_overlap.cu | build
 	$(NVCC) -O2 $(ARCH) -o $@ $<

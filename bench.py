@@ -402,6 +402,9 @@ class Ctx:
             if self.share:
                 dist.init_process_group("gloo")
             else:
+                # the NCCL log then shows the communicator's rank count (INIT lines only)
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
                 dist.init_process_group("nccl", device_id=torch.device("cuda", self.dev))
                 self.red_dev = "cuda"
             self.dist = dist
