@@ -494,18 +494,21 @@ def run_config(ctx, args, workload, steps, warmup, want_e2e=True):
     ctx.barrier()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = kg.launch_count()
     with ClockSampler(ctx.pci, ctx.dev) as clk:
         t_wall0 = time.perf_counter()
-        # A short device-side delay (untimed, before the start event) lets the
-        # host enqueue the first steps, so the device-timed region starts with
-        # work queued instead of idling through Python's first submit (the
-        # host-inclusive figure is `e2e`).
-        if args.queue_ahead_us > 0:
-            torch.cuda._sleep(int(args.queue_ahead_us * 1965))
+        # Q untimed steps between the barrier and the start event keep the GPU
+        # busy into the timed region: the device-timed region then starts with
+        # steps queued and the SMs at their steady-state speed, instead of idling
+        # through Python's first submit and re-warming for ~2 ms after the
+        # barrier's idle (profiles/r2_gpool).  The region holds exactly K steps;
+        # the host-inclusive figure is `e2e`.
+        ahead = [step() for _ in range(args.queue_ahead_steps)]
+        l0 = kg.launch_count()
         ev0.record(stream)
         tickets = [step() for _ in range(steps)]
         ev1.record(stream)
+        for t in ahead:
+            kg.wait(t)
         for t in tickets:
             kg.wait(t)
         torch.cuda.synchronize()
@@ -795,7 +798,10 @@ def run_ours(args):
         "config": {"workload": head["workload"], "name": args.workload, "n_pages_per_gpu": head["n_pages_per_gpu"],
                    "page_bytes": PB, "key_bits": head["key_bits"], "dir": head["dir"], "mode": head["mode"],
                    "residency": "hbm", "in_place": head["in_place"], "l2": head["l2"],
-                   "parallelism": f"page-range x{ctx.world}" if ctx.world > 1 else "1 GPU"},
+                   "parallelism": f"page-range x{ctx.world}" if ctx.world > 1 else "1 GPU",
+                   "timing": (f"{args.warmup} warm-up steps, barrier + synchronize, {args.queue_ahead_steps} untimed "
+                              f"queue-ahead steps, then CUDA events around exactly {args.steps} back-to-back steps "
+                              "on the launching stream; synchronize; max over ranks")},
         "roofline": head["roofline"],
         "e2e": head["e2e"],
         "gpu_launches": head["gpu_launches"],
@@ -866,8 +872,8 @@ def main(argv=None):
     ap.add_argument("--sweep-kmax", type=int, default=18)
     ap.add_argument("--sweep-nsk-pages", type=int, default=256)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--queue-ahead-us", type=float, default=200.0,
-                    help="device-side delay before the start event so the host can enqueue the first steps (0: off)")
+    ap.add_argument("--queue-ahead-steps", type=int, default=3,
+                    help="untimed steps enqueued after the barrier, right before the start event (0: none)")
     ap.add_argument("--ref-step-seconds", type=float, default=0.0,
                     help="reference arm: oracle seconds per step (default: sized so the run takes ~2.5 min)")
     args = ap.parse_args(argv)

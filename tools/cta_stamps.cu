@@ -13,6 +13,7 @@
 #include "../paper_1305_3345_b200/csrc/kg_kernels.cu"
 
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -53,13 +54,25 @@ int main(int argc, char **argv) {
     cudaMemcpyToSymbol(kg::g_stamp_ctr, &zero, 4);
     cudaStream_t st;
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    for (int rep = 0; rep < 12; rep++) kg::launch_pages(enc ? 0 : 1, 0, enc ? 14 : 10, a, 148, st);
+    // argv[2] = number of launches (default 12; with 8 the first launch, which
+    // follows an idle GPU, is in the record too)
+    const int nl = argc > 2 ? atoi(argv[2]) : 12;
+    cudaEvent_t ev0, ev1;
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0, st);
+    for (int rep = 0; rep < nl; rep++) kg::launch_pages(enc ? 0 : 1, 0, enc ? 14 : 10, a, 148, st);
+    cudaEventRecord(ev1, st);
     cudaStreamSynchronize(st);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    printf("{\"launches\": %d, \"event_ms\": %.4f, \"us_per_launch\": %.2f}\n", nl, ms, 1e3 * ms / nl);
     static unsigned long long h[8][148][kg::kStampW];
     cudaMemcpyFromSymbol(h, kg::g_stamps, sizeof h);
     const int warps = enc ? 32 : 16;
-    // launches 4..11 live in slots 4..7, 0..3
-    std::vector<int> order = {4, 5, 6, 7, 0, 1, 2, 3};
+    // the last 8 launches, oldest first (slot = launch index mod 8)
+    std::vector<int> order;
+    for (int k = (nl > 8 ? nl - 8 : 0); k < nl; k++) order.push_back(k & 7);
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < 148; c++) t0 = std::min(t0, h[order[0]][c][0]);
     double prev_last_done = -1, prev_first_wait = -1;
