@@ -500,7 +500,7 @@ def run_config(ctx, args, workload, steps, warmup, want_e2e=True):
         # busy into the timed region: the device-timed region then starts with
         # steps queued and the SMs at their steady-state speed, instead of idling
         # through Python's first submit and re-warming for ~2 ms after the
-        # barrier's idle (profiles/r2_gpool).  The region holds exactly K steps;
+        # barrier's idle (profiles/r2_timing).  The region holds exactly K steps;
         # the host-inclusive figure is `e2e`.
         ahead = [step() for _ in range(args.queue_ahead_steps)]
         l0 = kg.launch_count()
