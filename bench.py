@@ -686,25 +686,31 @@ def c4_sweep(ctx, args):
     except Exception:  # noqa: BLE001
         Cipher = None
 
-    def lat(fn, reps):
+    def lat(fn, reps, pct=False):
         ts = []
         for _ in range(reps):
             t0 = time.perf_counter()
             fn()
             ts.append(time.perf_counter() - t0)
-        return 1e6 * statistics.median(ts)
+        if not pct:
+            return 1e6 * statistics.median(ts)
+        q = np.percentile(np.array(ts) * 1e6, [10, 50, 90])
+        return [round(float(x), 2) for x in q]
 
     rows = []
     for k in range(kmax + 1):
         n = 1 << k
-        reps = 50 if n * PB < (1 << 20) else (20 if n * PB < (64 << 20) else 5)
+        reps = 50 if n * PB < (1 << 20) else 10    # >= 50 below 1 MiB, >= 10 above
         row = {"pages": n}
         for name, (a, b, c) in (("hbm", (dx, dout, div)), ("pinned", (hx, hout, hiv))):
             def f():
                 kg.wait(kg.submit_pages(1, 0, a, b, n, PB, c, 0, s))
             for _ in range(3):
                 f()
-            row[f"{name}_us"] = round(lat(f, reps), 2)
+            p10, p50, p90 = lat(f, reps, pct=True)
+            row[f"{name}_us"] = p50
+            row[f"{name}_us_p10_p90"] = [p10, p90]
+            row[f"{name}_gbs"] = round(n * PB / (p50 * 1e-6) / 1e9, 3)
         if n <= args.sweep_nsk_pages:
             kg.nsk_start(16, kg.NSK_DIRECT | kg.NSK_NOCAL, 5000)
 
@@ -749,11 +755,55 @@ def c4_sweep(ctx, args):
         for ck in ("oracle_1t_us", "oracle_T_us", "openssl_1core_us"):
             cross[f"{gk[:-3]} vs {ck[:-3]}"] = crossover(gk, ck)
     return {"workload": "C4 request batch-size sweep: AES-128-CBC decrypt, one request of 2^k 4 KiB pages, "
-                        f"k = 0..{kmax}; p50 latency in us (submit -> kg_wait returns)",
+                        f"k = 0..{kmax}; p50 latency in us (submit -> kg_wait returns, through Python), "
+                        "p10/p90 and GB/s at the p50 for the launch paths",
             "oracle_threads": threads, "rows": rows, "crossover": cross,
             "note": "crossover = smallest size from which the GPU p50 stays <= the CPU's (tie -> GPU); "
                     "openssl = single-core AES-NI via `cryptography`, context not the oracle; "
                     "the paper: GPU faster from 8 KB (PAPER.md:460-463)"}
+
+
+def c1_latency(ctx, args):
+    """configs[0] (C1): AES-128-CBC encrypt, then decrypt, of 16 seeded 4 KiB
+    pages in HBM; caller-observed latency of each direction (p10/p50/p90 over
+    200 requests) and the round trip; plus SP 800-38A F.2.1/F.2.2 (CBC-AES128
+    encrypt/decrypt) as one 64-byte page each, against the standard's values."""
+    import paper_1305_3345_b200 as kg
+    torch = ctx.torch
+    n = 16
+    kg.set_key(5, synth.make_key(16))
+    x = torch.from_numpy(synth.make_pages(n, PB)).cuda()
+    iv = torch.from_numpy(synth.make_ivs(n)).cuda()
+    c = torch.empty_like(x)
+    back = torch.empty_like(x)
+    s = torch.cuda.current_stream()
+    out = {"workload": "C1: AES-128-CBC encrypt then decrypt of 16 x 4 KiB pages (64 KiB), HBM, per-page IVs"}
+    for name, (d, a, b) in (("encrypt", (0, x, c)), ("decrypt", (1, c, back))):
+        ts = []
+        for r in range(210):
+            t0 = time.perf_counter()
+            kg.wait(kg.submit_pages(d, 0, a, b, n, PB, iv, 5, s))
+            if r >= 10:
+                ts.append(1e6 * (time.perf_counter() - t0))
+        out[f"{name}_us_p10_p50_p90"] = [round(float(v), 2) for v in np.percentile(ts, [10, 50, 90])]
+    torch.cuda.synchronize()
+    out["round_trip_equal"] = bool(torch.equal(back, x))
+    key = bytes.fromhex("2b7e151628aed2a6abf7158809cf4f3c")
+    pt = bytes.fromhex("6bc1bee22e409f96e93d7e117393172aae2d8a571e03ac9c9eb76fac45af8e51"
+                       "30c81c46a35ce411e5fbc1191a0a52eff69f2445df4f9b17ad2b417be66c3710")
+    ct = bytes.fromhex("7649abac8119b246cee98e9b12e9197d5086cb9b507219ee95db113a917678b2"
+                       "73bed6b8e3c1743b7116e69e222295163ff1caa1681fac09120eca307586e1a7")
+    kg.set_key(6, key)
+    tiv = torch.arange(16, dtype=torch.uint8).cuda()
+    tp = torch.frombuffer(bytearray(pt), dtype=torch.uint8).cuda()
+    tc = torch.empty_like(tp)
+    kg.wait(kg.submit_pages(0, 0, tp, tc, 1, 64, tiv, 6, s))
+    tb = torch.empty_like(tp)
+    kg.wait(kg.submit_pages(1, 0, tc, tb, 1, 64, tiv, 6, s))
+    torch.cuda.synchronize()
+    out["sp800_38a_f21_encrypt_ok"] = tc.cpu().numpy().tobytes() == ct
+    out["sp800_38a_f22_decrypt_ok"] = tb.cpu().numpy().tobytes() == pt
+    return out
 
 
 def run_ours(args):
@@ -781,8 +831,9 @@ def run_ours(args):
             if name not in WORKLOADS or name == args.workload:
                 continue
             extras[name] = run_config(ctx, args, name, args.steps, args.warmup)
-    sweep = None
+    sweep = c1 = None
     if ctx.world == 1 and not args.no_sweep and args.workload == "c2":
+        c1 = c1_latency(ctx, args)
         sweep = c4_sweep(ctx, args)
 
     if ctx.rank != 0:
@@ -812,6 +863,8 @@ def run_ours(args):
         "wall_s_timed": head["wall_s_timed"],
         "configs": extras,
     }
+    if c1:
+        line["c1"] = c1
     if sweep:
         line["c4_sweep"] = sweep
     if ctx.world == 1 and not args.no_cpu_baseline:

@@ -61,3 +61,7 @@ def test_bench_one_gpu_line_contract():
     rows = d["c4_sweep"]["rows"]
     assert [r["pages"] for r in rows] == [1 << k for k in range(7)]
     assert all(r["hbm_us"] > 0 and r["pinned_us"] > 0 for r in rows)
+    assert all(r["hbm_us_p10_p90"][0] <= r["hbm_us"] <= r["hbm_us_p10_p90"][1] for r in rows)
+    c1 = d["c1"]
+    assert c1["round_trip_equal"] and c1["sp800_38a_f21_encrypt_ok"] and c1["sp800_38a_f22_decrypt_ok"]
+    assert 0 < c1["decrypt_us_p10_p50_p90"][1] < 1e4
