@@ -579,28 +579,56 @@ def run_config(ctx, args, workload, steps, warmup, want_e2e=True):
         hx.copy_(x)
         hiv = kg.alloc_pinned(16 * n)
         hiv.copy_(ivs)
-        hout = hx if in_place else kg.alloc_pinned(n * PB)
+        # Requests in flight: like the paper's pipelined service calls (one
+        # buffer in service while the next is copied in and the previous out,
+        # PAPER.md:437-440), the caller keeps `depth` batches submitted and
+        # waits for the oldest; each batch in flight has its own output buffer
+        # (nothing is shared between batches in flight).  In place (C5) the
+        # next batch's input is the previous one's output: one at a time.
+        depth = 1 if in_place else max(1, args.e2e_depth)
+        houts = [hx] if in_place else [kg.alloc_pinned(n * PB) for _ in range(depth)]
         del x, out, ivs
         torch.cuda.empty_cache()
         residency = ("pinned host (kg_alloc_pinned: cudaHostAlloc from a thread on the GPU-local CPUs)"
-                     + (", in place" if in_place else ""))
-        for _ in range(1 if big else 2):
-            kg.wait(kg.submit_pages(direction, mode, hx, hout, n, PB, hiv if mode == 0 else None, 0, stream))
+                     + (", in place" if in_place else f", {depth} batches in flight, one output buffer each"))
+
+        # each batch in flight on its own stream: a batch is ordered after the
+        # work already on its stream (kg.h), so one stream would serialise them
+        e_streams = [stream] + [torch.cuda.Stream() for _ in range(depth - 1)]
+
+        def submit_e2e(i):
+            return kg.submit_pages(direction, mode, hx, houts[i % depth], n, PB, hiv if mode == 0 else None, 0,
+                                   e_streams[i % depth])
+
+        for i in range(1 if big else 2):
+            kg.wait(submit_e2e(i))
         ctx.barrier()
         step_ms = []
         t0 = time.perf_counter()
-        for _ in range(e_steps):
-            ts = time.perf_counter()
-            kg.wait(kg.submit_pages(direction, mode, hx, hout, n, PB, hiv if mode == 0 else None, 0, stream))
-            step_ms.append((time.perf_counter() - ts) * 1e3)
+        inflight = []
+        t_prev = t0
+        for i in range(e_steps):
+            if len(inflight) == depth:
+                kg.wait(inflight.pop(0))
+                t_now = time.perf_counter()
+                step_ms.append((t_now - t_prev) * 1e3)
+                t_prev = t_now
+            inflight.append(submit_e2e(i))
+        for t in inflight:
+            kg.wait(t)
+            t_now = time.perf_counter()
+            step_ms.append((t_now - t_prev) * 1e3)
+            t_prev = t_now
         te = time.perf_counter() - t0
         te_max = reduce_max(ctx.dist, [te], ctx.red_dev)[0]
         e2e = {"value": job_bytes(workload, ctx.world, e_steps) / te_max / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": n * PB + (16 * n if mode == 0 else 0), "d2h_bytes_per_step": n * PB,
-               "steps": e_steps, "residency": residency, "timing": "wall clock around submit + kg_wait, max over ranks",
+               "steps": e_steps, "residency": residency, "batches_in_flight": depth,
+               "timing": "wall clock from the first submit to the last kg_wait, max over ranks; step_ms = intervals "
+                         "between successive completions",
                "step_ms_min_median_max": [round(min(step_ms), 3), round(sorted(step_ms)[len(step_ms) // 2], 3),
                                           round(max(step_ms), 3)]}
-        per_rank, agg = duplex_link(torch, ctx.dist, ctx.red_dev, hx, hout)
+        per_rank, agg = duplex_link(torch, ctx.dist, ctx.red_dev, hx, houts[0])
         e2e["link_duplex_gbs_per_direction"] = per_rank
         e2e["link_duplex_aggregate_gbs_per_direction"] = agg
         e2e["link_frac"] = e2e["value"] / agg if agg else None
@@ -609,8 +637,9 @@ def run_config(ctx, args, workload, steps, warmup, want_e2e=True):
         kg.free_pinned(hx)
         kg.free_pinned(hiv)
         if not in_place:
-            kg.free_pinned(hout)
-        del hx, hout, hiv
+            for h in houts:
+                kg.free_pinned(h)
+        del hx, houts, hiv
     else:
         del x, out, ivs
     del key_ids
@@ -918,6 +947,8 @@ def main(argv=None):
     ap.add_argument("--extra", default="default",
                     help="comma list of extra workloads in the same line (with --workload c2); 'none' to skip")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-depth", type=int, default=3,
+                    help="e2e: batches the caller keeps in flight (out-of-place workloads; 1 = submit, wait, repeat)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")

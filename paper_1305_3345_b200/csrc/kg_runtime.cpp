@@ -148,6 +148,7 @@ struct Ctx {
     // D2H, profiles/r1_pinned/README.md
     uint64_t chunk_bytes = 0;
     int n_slots = 4;
+    uint64_t slot_next = 0;    // slot of the next staged chunk (rotation continues across batches)
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
     // batch IVs of host batches (<= kIvStageMax), double-buffered: a buffer is
@@ -608,10 +609,16 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         return lag && j + 1 < sched.size() && (lag_mode == 1 || (lag_mode == 2 && sched[j + 1] == sched[j]) ||
                                                (lag_mode == 3 && j + 2 < sched.size()));
     };
+    // The slot rotation continues across batches: batch k+1's first chunk takes
+    // the slot after batch k's last one, so its H2D waits only for a D2H a few
+    // chunks back instead of batch k's final D2H, and batches submitted back
+    // to back (on different caller streams) keep the copy engines busy.
+    const uint64_t base = g.slot_next;
+    g.slot_next += sched.size();
     auto d2h = [&](uint64_t j, uint64_t pj) -> int {  // D2H stage of chunk j (first page pj)
-        Slot &s = g.slots[j % (uint64_t)g.n_slots];
+        Slot &s = g.slots[(base + j) % (uint64_t)g.n_slots];
         KG_CU(cudaStreamWaitEvent(g.s_d2h, s.done, 0));
-        if (lag_on(j)) KG_CU(cudaStreamWaitEvent(g.s_d2h, g.slots[(j + 1) % (uint64_t)g.n_slots].loaded, 0));
+        if (lag_on(j)) KG_CU(cudaStreamWaitEvent(g.s_d2h, g.slots[(base + j + 1) % (uint64_t)g.n_slots].loaded, 0));
         if (kout == K_HOST)
             KG_CU(cudaMemcpyAsync(out + pj * page_bytes, s.data, sched[j] * page_bytes, cudaMemcpyDeviceToHost,
                                   g.s_d2h));
@@ -623,7 +630,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     for (uint64_t i = 0; i < sched.size(); p_prev = p0, p0 += sched[i], ++i) {
         const uint64_t np = sched[i];
         const uint64_t off = p0 * page_bytes, nbytes = np * page_bytes;
-        Slot &s = g.slots[i % (uint64_t)g.n_slots];
+        Slot &s = g.slots[(base + i) % (uint64_t)g.n_slots];
         NvtxRange nv_chunk("kg staged chunk (H2D, kernel, D2H enqueue)");
         // H2D stage: wait until the slot's previous output has drained.
         KG_CU(cudaStreamWaitEvent(g.s_h2d, s.freed, 0));

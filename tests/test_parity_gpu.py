@@ -239,7 +239,7 @@ def test_texture_path_variants(env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_parity_gpu.py"),
-                        "-k", "(cbc_device or ecb or tail_pool) and not texture_path"],
+                        "-k", "(cbc_device or ecb or tail_pool or mixed_residency or one_batch_texture) and not texture_path"],
                        cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
@@ -272,3 +272,32 @@ def test_texture_cache_eviction_many_buffers_and_streams():
         torch.cuda.synchronize()
         exp = oracle_pages(1, 0, key, data, n, pb, ivs)
         assert first_mismatch(out.cpu().numpy(), exp) is None
+
+
+@pytest.mark.parametrize("direction,mode", [(1, 0), (0, 0), (1, 1), (0, 1)])
+def test_staged_device_input_one_batch_texture(direction, mode):
+    """Device input, pinned output, staged in many small chunks: every chunk's
+    launch reads its slice of ONE texture over the whole batch input
+    (a texture per chunk missed the cache every chunk); in
+    KG_TEX_MAX_ELEMS runs (test_texture_path_variants) the batch exceeds one
+    texture and the chunks fall back to their own textures."""
+    from gpu_util import kg_ready, put
+    kg, torch = kg_ready()
+    n, pb = 300, 4096
+    key = synth.make_key(16, seed=515)
+    kg.set_key(0, key)
+    data = synth.make_pages(n, pb, seed=516)
+    ivs = synth.make_ivs(n, seed=517) if mode == 0 else None
+    exp = oracle_pages(direction, mode, key, data, n, pb, ivs)
+    x = put(torch, data, "device")
+    iv = None if ivs is None else put(torch, ivs, "device")
+    out = torch.empty(n * pb, dtype=torch.uint8).pin_memory()
+    kg.set_host_path(kg.HOST_STAGED, 0)
+    kg.set_pipeline(16 * pb, 3)          # 19 chunks
+    try:
+        kg.wait(kg.submit_pages(direction, mode, x, out, n, pb, iv, 0))
+    finally:
+        kg.set_pipeline(0, 4)
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)
+    torch.cuda.synchronize()
+    assert first_mismatch(out.numpy(), exp) is None
