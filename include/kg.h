@@ -167,7 +167,8 @@ KG_API const char *kg_strerror(int status);
  *                    launches of batches larger than one texture, 2^28 texels)
  *   KG_D2H_LAG=0|2|3 staged D2H not held back / only between equal chunks /
  *                    not for the last two chunks
- *   KG_RAMP_DOWN=0..3  end-ramp levels of the staging schedule (default 3)
+ *   KG_RAMP_DOWN=0..3  end-ramp levels of a cold batch's staging schedule (default 3)
+ *   KG_RAMP_WARM=0   treat every staged batch as cold (ramps, 8 MiB auto chunks)
  *   KG_KEYED=0|1     mixed-key kernels: one block per lane / __ldg round keys
  *   KG_PAIR=0        one block per lane instead of block pairs
  *   KG_PDL=0         no programmatic dependent launch
@@ -175,9 +176,11 @@ KG_API const char *kg_strerror(int status);
  *   KG_NSK_STAMPS=1  NSK per-request %globaltimer stamps;  KG_DEBUG=1 CUDA errors */
 
 /* Staging pipeline for batches touching host memory: chunk size in bytes
- * (rounded down to whole pages, at least one page; 0 = auto: 8 MiB, or
- * 16 MiB for CBC encryption, whose per-page chains need the longer copy to
- * hide behind) and number of device staging slots (2..8).  Takes effect for
+ * (rounded down to whole pages, at least one page; 0 = auto: 8 MiB with
+ * ramped first/last chunks when the copy engines are idle at submit, 16 MiB
+ * without ramps when earlier batches' copies are still queued, and 16 MiB for
+ * CBC encryption, whose per-page chains need the longer copy to hide behind)
+ * and number of device staging slots (2..8).  Takes effect for
  * later submits.  Defaults: auto, 4 slots (PAPER.md:437-440's "three
  * buffers" plus one: the D2H of a chunk is held back until the next chunk's
  * H2D has landed, profiles/r1_lag).  Environment overrides at kg_init:

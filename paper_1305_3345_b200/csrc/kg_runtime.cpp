@@ -142,10 +142,11 @@ struct Ctx {
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_begin = nullptr;
     Slot slots[kMaxSlots];
-    // 0 = auto: 8 MiB for block-parallel kernels, 16 MiB for CBC-encrypt
-    // chains (whose per-chunk kernel is latency-bound at ~90 us below ~74 MiB,
-    // so it needs the longer copy to hide behind); measured with the lagged
-    // D2H, profiles/r1_pinned/README.md
+    // 0 = auto: 8 MiB for block-parallel kernels (16 MiB when the pipeline is
+    // warm, submit_staged), 16 MiB for CBC-encrypt chains (whose per-chunk
+    // kernel is latency-bound at ~90 us below ~74 MiB, so it needs the longer
+    // copy to hide behind); measured with the lagged D2H,
+    // profiles/r1_pinned/README.md, profiles/r2_e2e
     uint64_t chunk_bytes = 0;
     int n_slots = 4;
     uint64_t slot_next = 0;    // slot of the next staged chunk (rotation continues across batches)
@@ -528,13 +529,36 @@ int ensure_iv_stage(int b, uint64_t bytes) {
 int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint8_t *in, Kind kin,
                   uint8_t *out, Kind kout, uint64_t n_pages, uint32_t page_bytes, const uint8_t *ivs,
                   Kind kiv, cudaStream_t st, const kg::KeyedArgs *keyed = nullptr) {
+    // Warm pipeline: H2D copies of earlier batches are still queued (queried
+    // before this batch adds its own work).  A cold batch is latency-bound by
+    // its fill and drain (small chunks and ramps, below); a warm one by the
+    // link, where fewer, larger copies win: auto chunk 8 MiB cold / 16 MiB warm
+    // for the block-parallel kernels (C2 e2e 0.91 -> 0.97 of the duplex link
+    // with batches back to back, profiles/r2_e2e).  KG_RAMP_WARM=0: always cold.
+    static const bool warm_skip = [] {
+        const char *e = getenv("KG_RAMP_WARM");
+        return !(e && *e == '0');
+    }();
+    bool warm = false;
+    if (warm_skip) {
+        warm = cudaStreamQuery(g.s_h2d) == cudaErrorNotReady;
+        cudaGetLastError();
+    }
     const uint64_t cb = g.chunk_bytes ? g.chunk_bytes
-                        : (dir == KG_ENCRYPT && mode == KG_MODE_CBC) ? (16ull << 20) : (8ull << 20);
+                        : (dir == KG_ENCRYPT && mode == KG_MODE_CBC) || warm ? (16ull << 20) : (8ull << 20);
     uint64_t chunk_pages = cb / page_bytes;
     if (chunk_pages < 1) chunk_pages = 1;
     if (chunk_pages > n_pages) chunk_pages = n_pages;
     const bool need_iv = (mode == KG_MODE_CBC);
-    int rc = ensure_staging(chunk_pages * page_bytes, need_iv ? chunk_pages * 16 : 16);
+    // auto chunks: size the slots for the warm (larger) chunk from the start,
+    // so that a batch turning warm does not drain the pipeline to grow them
+    uint64_t slot_pages = chunk_pages;
+    if (!g.chunk_bytes) {
+        uint64_t wp = (16ull << 20) / page_bytes;
+        if (wp > n_pages) wp = n_pages;
+        if (wp > slot_pages) slot_pages = wp;
+    }
+    int rc = ensure_staging(slot_pages * page_bytes, need_iv ? slot_pages * 16 : 16);
     if (rc != KG_OK) return rc;
 
     // Device-memory input read through the texture pipe: ONE texture over the
@@ -568,20 +592,29 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     // Chunk schedule.  The first H2D and the last D2H overlap nothing, so for
     // batches of >= 4 chunks the ends ramp C/8, C/4, C/2 (... C ...) C/2, C/4,
     // C/8: fill and drain shrink 8x for a few extra chunks (profiles/r1_pinned).
+    // Only for a cold pipeline: a batch submitted while earlier H2D copies are
+    // still queued uses full chunks throughout (profiles/r2_e2e).
     std::vector<uint64_t> sched;
     {
         uint64_t left = n_pages;
         std::vector<uint64_t> ramp;
+        // The ramp-up only shortens an idle pipeline's fill: when earlier H2D
+        // copies are still queued (batches back to back) this batch's first
+        // copy waits behind them anyway, and the small chunks only add per-copy
+        // cost, so a warm pipeline starts with full chunks (KG_RAMP_WARM=0: always ramp).
         if (n_pages >= 4 * chunk_pages && chunk_pages >= 8)
             for (uint64_t d = 8; d >= 2; d /= 2) ramp.push_back(chunk_pages / d);
         // KG_RAMP_DOWN = number of ramp levels at the end (0..3, default 3:
-        // C/2, C/4, C/8); the ramp-up is always C/8, C/4, C/2
+        // C/2, C/4, C/8); the ramp-up is C/8, C/4, C/2 unless warm
         static const size_t down = [] {
             const char *e = getenv("KG_RAMP_DOWN");
             return (e && *e >= '0' && *e <= '3') ? (size_t)(*e - '0') : (size_t)3;
         }();
-        const size_t nd = down < ramp.size() ? down : ramp.size();
-        for (uint64_t r : ramp) sched.push_back(r), left -= r;
+        // a warm pipeline (batches back to back) skips the ramp-down too: the
+        // next batch's copies fill the drain (measured, profiles/r2_e2e)
+        const size_t nd = warm ? 0 : down < ramp.size() ? down : ramp.size();
+        if (!warm)
+            for (uint64_t r : ramp) sched.push_back(r), left -= r;
         for (size_t r = ramp.size() - nd; r < ramp.size(); ++r) left -= ramp[r];
         std::vector<uint64_t> mid;
         while (left > 0) {

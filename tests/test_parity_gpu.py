@@ -189,6 +189,42 @@ def test_staged_batches_back_to_back():
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
 
 
+def test_staged_auto_chunks_warm_and_cold():
+    """Auto chunking: a batch submitted while earlier batches' copies are still
+    queued runs warm (16 MiB chunks, no ramps), one submitted to idle copy
+    engines cold (8 MiB chunks, ramped ends); slots are sized for the warm
+    chunk from the start.  Batches of 9,000 x 4 KiB pages (ragged against both
+    chunk sizes) on separate streams, both directions, every byte vs the oracle."""
+    from gpu_util import kg_ready
+    kg, torch = kg_ready()
+    kg.set_host_path(kg.HOST_STAGED)
+    kg.set_pipeline(0, 4)
+    try:
+        n, pb = 9000, 4096
+        key = synth.make_key(32, seed=811)
+        kg.set_key(0, key)
+        streams = [torch.cuda.Stream() for _ in range(3)]
+        jobs = []
+        for b in range(5):
+            data = synth.make_pages(n, pb, seed=820 + b)
+            ivs = synth.make_ivs(n, seed=830 + b)
+            d = (b + 1) % 2
+            hin = torch.from_numpy(data).pin_memory()
+            hiv = torch.from_numpy(ivs).pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            t = kg.submit_pages(d, 0, hin, hout, n, pb, hiv, 0, streams[b % 3])
+            jobs.append((t, d, data, ivs, hout, hin, hiv))
+            if b == 3:  # let the pipeline go idle: the last batch is cold again
+                kg.wait(t)
+        for t, d, data, ivs, hout, *_ in jobs:
+            if t != jobs[3][0]:
+                kg.wait(t)
+            exp = oracle_pages(d, 0, key, data, n, pb, ivs)
+            assert first_mismatch(hout.numpy(), exp) is None
+    finally:
+        kg.set_host_path(kg.HOST_AUTO, 32 << 20)
+
+
 @pytest.mark.parametrize("pb", [1056, 4096, 2080])
 @pytest.mark.parametrize("inplace", [False, True])
 def test_tail_pool_large_batches(pb, inplace):
