@@ -44,7 +44,7 @@ build/kgpu_crypt: examples/kgpu_crypt.c include/kg.h $(LIB) | build
 
 # diagnostics (not part of `all`): copy-engine overlap, per-CTA stamps, bitsliced round
 tools: build/zc_duplex build/bitslice_bp build/copy_overlap build/cta_stamps build/bitslice_bench build/soak_tsan build/pipes_tex build/pipes_lds build/pipes_ldpath \
-       build/hybrid_bench build/pipe_variants
+       build/hybrid_bench build/hybrid_throttle build/pipe_variants
 
 build/zc_duplex: tools/zc_duplex.cu | build
 	$(NVCC) -O2 -std=c++17 $(ARCH) -o $@ $<
@@ -62,6 +62,9 @@ build/pipes_tex build/pipes_lds build/pipes_ldpath: build/%: tools/%.cu | build
 	$(NVCC) -O3 -std=c++17 $(ARCH) -o $@ $<
 
 build/hybrid_bench: tools/hybrid_bench.cu tools/kg_sbox_bs.cuh | build
+	$(NVCC) -O3 -std=c++17 $(ARCH) -Itools -o $@ $<
+
+build/hybrid_throttle: tools/hybrid_throttle.cu tools/kg_sbox_bp.cuh | build
 	$(NVCC) -O3 -std=c++17 $(ARCH) -Itools -o $@ $<
 
 build/pipe_variants: tools/pipe_variants.cu | build

@@ -177,8 +177,9 @@ KG_API const char *kg_strerror(int status);
 
 /* Staging pipeline for batches touching host memory: chunk size in bytes
  * (rounded down to whole pages, at least one page; 0 = auto: 8 MiB with
- * ramped first/last chunks when the copy engines are idle at submit, 16 MiB
- * without ramps when earlier batches' copies are still queued, and 16 MiB for
+ * ramped first/last chunks when the copy engines are idle at submit (16 MiB
+ * for batches of 1 GiB or more), 16 MiB without ramps when earlier batches'
+ * copies are still queued, and 16 MiB for
  * CBC encryption, whose per-page chains need the longer copy to hide behind)
  * and number of device staging slots (2..8).  Takes effect for
  * later submits.  Defaults: auto, 4 slots (PAPER.md:437-440's "three

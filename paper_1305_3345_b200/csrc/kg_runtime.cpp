@@ -530,11 +530,13 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
                   uint8_t *out, Kind kout, uint64_t n_pages, uint32_t page_bytes, const uint8_t *ivs,
                   Kind kiv, cudaStream_t st, const kg::KeyedArgs *keyed = nullptr) {
     // Warm pipeline: H2D copies of earlier batches are still queued (queried
-    // before this batch adds its own work).  A cold batch is latency-bound by
-    // its fill and drain (small chunks and ramps, below); a warm one by the
-    // link, where fewer, larger copies win: auto chunk 8 MiB cold / 16 MiB warm
-    // for the block-parallel kernels (C2 e2e 0.91 -> 0.97 of the duplex link
-    // with batches back to back, profiles/r2_e2e).  KG_RAMP_WARM=0: always cold.
+    // before this batch adds its own work).  A cold batch below 1 GiB is
+    // bound by its fill and drain (small chunks and ramps, below); a warm or
+    // a large one by the link, where fewer, larger copies win: auto chunk
+    // 8 MiB cold / 16 MiB warm or >= 1 GiB for the block-parallel kernels
+    // (C2 e2e 0.91 -> 0.95-0.97 of the duplex link with batches back to back;
+    // one 64 GiB C5 batch 0.96 -> 0.98; profiles/r2_e2e).  KG_RAMP_WARM=0:
+    // always cold.
     static const bool warm_skip = [] {
         const char *e = getenv("KG_RAMP_WARM");
         return !(e && *e == '0');
@@ -545,7 +547,9 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         cudaGetLastError();
     }
     const uint64_t cb = g.chunk_bytes ? g.chunk_bytes
-                        : (dir == KG_ENCRYPT && mode == KG_MODE_CBC) || warm ? (16ull << 20) : (8ull << 20);
+                        : (dir == KG_ENCRYPT && mode == KG_MODE_CBC) || warm || n_pages * page_bytes >= (1ull << 30)
+                            ? (16ull << 20)
+                            : (8ull << 20);
     uint64_t chunk_pages = cb / page_bytes;
     if (chunk_pages < 1) chunk_pages = 1;
     if (chunk_pages > n_pages) chunk_pages = n_pages;

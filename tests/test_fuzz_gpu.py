@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 def test_random_cases():
     kg, torch = kg_ready()
-    # KG_FUZZ_CASES / KG_FUZZ_SEED: longer soak runs (tools/gpu_fuzz_soak.sh)
+    # KG_FUZZ_CASES / KG_FUZZ_SEED: longer soak runs (tools/runs/gpu_fuzz_soak.sh)
     rng = np.random.default_rng(int(os.environ.get("KG_FUZZ_SEED", "20261017")))
     for case in range(int(os.environ.get("KG_FUZZ_CASES", "150"))):
         d = int(rng.integers(0, 2))
