@@ -24,7 +24,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
+#include "kg_inv_sbox_bp.cuh"
 #include "kg_sbox_bp.cuh"
 
 __constant__ uint32_t c_rk[128];
@@ -73,9 +75,93 @@ __device__ __forceinline__ void bs_round(uint32_t *s) {
     }
 }
 
+// Inverse round (FIPS-197 §5.3 InvCipher order): InvShiftRows (renaming),
+// InvSubBytes (tools/kg_inv_sbox_bp.cuh), AddRoundKey, InvMixColumns as
+// MixColumns after the 04-multiple pre-step (a0 ^= 04(a0^a2), a2 likewise,
+// a1 ^= 04(a1^a3), a3 likewise).
+// Pin 8 values at this point of the (volatile-ordered) schedule: S-boxes
+// bracketed by pins run one after another, which bounds the live registers
+// (ptxas otherwise interleaves several S-boxes and spills).
+__device__ __forceinline__ void pin8(uint32_t *x) {
+    asm volatile("" : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]));
+}
+
+__device__ __forceinline__ void bs_inv_round(uint32_t *s) {
+    // InvSubBytes commutes with InvShiftRows: S-boxes in place on s first
+#pragma unroll
+    for (int byte = 0; byte < 16; byte++) {
+        pin8(s + 8 * byte);
+        bs_inv_sbox_bp(s + 8 * byte);
+        pin8(s + 8 * byte);
+    }
+    uint32_t t[128];
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int b = 0; b < 8; b++)
+                t[(c * 4 + r) * 8 + b] = s[(((c - r + 4) & 3) * 4 + r) * 8 + b] ^ c_rk[(c * 4 + r) * 8 + b];
+    // InvMixColumns = MixColumns(e) with e_r = a_r ^ (r even ? U : V),
+    // U = 04(a0^a2), V = 04(a1^a3).  The e sum equals the a sum T, and
+    // e_r ^ e_{r+1} = a_r ^ a_{r+1} ^ U ^ V, so
+    //   out_r = a_r ^ 02(a_r ^ a_{r+1}) ^ T ^ 02(U ^ V) ^ (r even ? U : V).
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const uint32_t *a = t + c * 32;
+        uint32_t TU[8], TV[8];
+        {
+            uint32_t u[8], x1[8], U[8], V[8], W[8];
+#pragma unroll
+            for (int b = 0; b < 8; b++) u[b] = a[b] ^ a[16 + b];
+            xtime8(u, x1);
+            xtime8(x1, U);
+#pragma unroll
+            for (int b = 0; b < 8; b++) u[b] = a[8 + b] ^ a[24 + b];
+            xtime8(u, x1);
+            xtime8(x1, V);
+#pragma unroll
+            for (int b = 0; b < 8; b++) u[b] = U[b] ^ V[b];
+            xtime8(u, W);
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                const uint32_t T = a[b] ^ a[8 + b] ^ a[16 + b] ^ a[24 + b] ^ W[b];
+                TU[b] = T ^ U[b];
+                TV[b] = T ^ V[b];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            uint32_t w[8], y2[8];
+#pragma unroll
+            for (int b = 0; b < 8; b++) w[b] = a[r * 8 + b] ^ a[((r + 1) & 3) * 8 + b];
+            xtime8(w, y2);
+#pragma unroll
+            for (int b = 0; b < 8; b++) s[(c * 4 + r) * 8 + b] = a[r * 8 + b] ^ y2[b] ^ ((r & 1) ? TV[b] : TU[b]);
+        }
+    }
+}
+
+// one thread: a bitsliced inverse round on 32 blocks in[32][16] -> out[32][16]
+__global__ void k_check_inv(const uint8_t *in, uint8_t *out) {
+    if (threadIdx.x != 0) return;
+    uint32_t s[128];
+    for (int i = 0; i < 128; i++) s[i] = 0;
+    for (int j = 0; j < 32; j++)
+        for (int k = 0; k < 16; k++)  // byte k = row k%4, column k/4 (FIPS-197 §3.4)
+            for (int b = 0; b < 8; b++) s[((k >> 2) * 4 + (k & 3)) * 8 + b] |= (uint32_t)((in[16 * j + k] >> b) & 1) << j;
+    bs_inv_round(s);
+    for (int j = 0; j < 32; j++)
+        for (int k = 0; k < 16; k++) {
+            int v = 0;
+            for (int b = 0; b < 8; b++) v |= ((s[((k >> 2) * 4 + (k & 3)) * 8 + b] >> j) & 1) << b;
+            out[16 * j + k] = (uint8_t)v;
+        }
+}
+
 // NBS: bitsliced warps of warpgroup 3 (0..4); TT3: WG3's other warps run
 // T-table rounds (else they exit at once)
-template <int NTT_WG, int NBS, int SLEEP_SBOX, int SLEEP_ROUND, bool TT3 = false>
+template <int NTT_WG, int NBS, int SLEEP_SBOX, int SLEEP_ROUND, bool TT3 = false, bool INV = false>
 __global__ void __launch_bounds__(512, 1) k_hybrid(unsigned long long ns, unsigned long long *cnt, uint32_t *sink) {
     extern __shared__ __align__(16) char smc[];
     for (int i = threadIdx.x; i < 32768; i += blockDim.x) reinterpret_cast<uint32_t *>(smc)[i] = i * 2654435761u;
@@ -123,8 +209,10 @@ __global__ void __launch_bounds__(512, 1) k_hybrid(unsigned long long ns, unsign
         uint32_t s[128];
 #pragma unroll
         for (int i = 0; i < 128; i++) s[i] = (threadIdx.x + 1) * (i + 7) * 2654435761u;
+#pragma unroll 1
         for (;;) {
-            bs_round<SLEEP_SBOX>(s);
+            if (INV) bs_inv_round(s);
+            else bs_round<SLEEP_SBOX>(s);
             if (SLEEP_ROUND > 0) __nanosleep(SLEEP_ROUND);
             rounds += 32 * 32;  // 32 blocks per thread
             unsigned long long g;
@@ -143,13 +231,13 @@ __global__ void __launch_bounds__(512, 1) k_hybrid(unsigned long long ns, unsign
     if (threadIdx.x == 0) atomicMax(&cnt[2], c1 - c0);
 }
 
-template <int NTT_WG, int NBS, int SLEEP_SBOX, int SLEEP_ROUND, bool TT3 = false>
+template <int NTT_WG, int NBS, int SLEEP_SBOX, int SLEEP_ROUND, bool TT3 = false, bool INV = false>
 static void run(int sms, const char *name) {
     unsigned long long *cnt;
     uint32_t *sink;
     cudaMalloc(&cnt, 32);
     cudaMalloc(&sink, 4);
-    auto k = k_hybrid<NTT_WG, NBS, SLEEP_SBOX, SLEEP_ROUND, TT3>;
+    auto k = k_hybrid<NTT_WG, NBS, SLEEP_SBOX, SLEEP_ROUND, TT3, INV>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, k);
@@ -161,17 +249,74 @@ static void run(int sms, const char *name) {
     unsigned long long h[4];
     cudaMemcpy(h, cnt, 32, cudaMemcpyDeviceToHost);
     const double clk = (double)h[2];
-    printf("{\"test\": \"hybrid_throttle\", \"arm\": \"%s\", \"ttable_warps\": %d, \"bitsliced_warps\": %d, "
+    printf("{\"test\": \"hybrid_throttle\", \"arm\": \"%s%s\", \"ttable_warps\": %d, \"bitsliced_warps\": %d, "
            "\"sleep_ns_per_sbox\": %d, \"sleep_ns_per_round\": %d, \"regs\": %d, \"local_bytes\": %zu, "
            "\"ttable_block_rounds_per_clk_sm\": %.4f, \"bitsliced_block_rounds_per_clk_sm\": %.4f, \"total\": %.4f, "
            "\"cycles\": %.0f}\n",
-           name, 4 * NTT_WG + (TT3 ? 4 - NBS : 0), NBS, SLEEP_SBOX, SLEEP_ROUND, fa.numRegs, (size_t)fa.localSizeBytes, h[0] / clk / sms,
+           name, INV ? "_inverse" : "", 4 * NTT_WG + (TT3 ? 4 - NBS : 0), NBS, SLEEP_SBOX, SLEEP_ROUND, fa.numRegs, (size_t)fa.localSizeBytes, h[0] / clk / sms,
            h[1] / clk / sms, (h[0] + h[1]) / clk / sms, clk);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e));
     fflush(stdout);
     cudaFree(cnt);
     cudaFree(sink);
+}
+
+// host byte-oriented reference of one inverse round (for the device check)
+static uint8_t gmul(uint8_t a, uint8_t b) {
+    uint8_t p = 0;
+    for (int i = 0; i < 8; i++) {
+        if (b & 1) p ^= a;
+        const uint8_t hi = a & 0x80;
+        a <<= 1;
+        if (hi) a ^= 0x1b;
+        b >>= 1;
+    }
+    return p;
+}
+
+static bool check_inverse_round(const uint32_t *rk) {
+    uint8_t sbox[256], isb[256];
+    for (int x = 0; x < 256; x++) {
+        uint8_t inv = 0;
+        for (int y = 1; y < 256 && x; y++)
+            if (gmul((uint8_t)x, (uint8_t)y) == 1) inv = (uint8_t)y;
+        uint8_t b = inv, r = inv;
+        for (int i = 0; i < 4; i++) {
+            r = (uint8_t)((r << 1) | (r >> 7));
+            b ^= r;
+        }
+        sbox[x] = b ^ 0x63;
+    }
+    for (int x = 0; x < 256; x++) isb[sbox[x]] = (uint8_t)x;
+    uint8_t in[512], out[512], exp[512], key[16];
+    for (int i = 0; i < 512; i++) in[i] = (uint8_t)(i * 131 + 7 + (i >> 4) * 29);
+    for (int k = 0; k < 16; k++) {
+        key[k] = 0;
+        for (int b = 0; b < 8; b++) key[k] |= (uint8_t)((rk[k * 8 + b] & 1) << b);
+    }
+    for (int j = 0; j < 32; j++) {
+        const uint8_t *o = in + 16 * j;
+        uint8_t t[16];
+        for (int c = 0; c < 4; c++)
+            for (int r = 0; r < 4; r++) t[r + 4 * c] = isb[o[r + 4 * ((c - r + 4) & 3)]] ^ key[r + 4 * c];
+        for (int c = 0; c < 4; c++)
+            for (int r = 0; r < 4; r++)
+                exp[16 * j + r + 4 * c] = gmul(t[r + 4 * c], 14) ^ gmul(t[(r + 1) % 4 + 4 * c], 11) ^
+                                          gmul(t[(r + 2) % 4 + 4 * c], 13) ^ gmul(t[(r + 3) % 4 + 4 * c], 9);
+    }
+    uint8_t *d_in, *d_out;
+    cudaMalloc(&d_in, 512);
+    cudaMalloc(&d_out, 512);
+    cudaMemcpy(d_in, in, 512, cudaMemcpyHostToDevice);
+    k_check_inv<<<1, 32>>>(d_in, d_out);
+    cudaMemcpy(out, d_out, 512, cudaMemcpyDeviceToHost);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    int bad = 0;
+    for (int i = 0; i < 512; i++) bad += out[i] != exp[i];
+    printf("{\"check\": \"bitsliced_inverse_round\", \"byte_mismatches\": %d}\n", bad);
+    return bad == 0;
 }
 
 int main() {
@@ -181,6 +326,15 @@ int main() {
     for (int i = 0; i < 128; i++) rk[i] = (i * 2654435761u) & 0x10 ? 0xffffffffu : 0u;
     cudaMemcpyToSymbol(c_rk, rk, sizeof rk);
     const int sms = p.multiProcessorCount;
+    check_inverse_round(rk);
+    if (getenv("HYB_INV_ONLY")) {
+        run<4, 0, 0, 0>(sms, "ttable_16w");
+        run<3, 2, 0, 0, true, true>(sms, "hybrid_14tt_2bs");
+        run<3, 3, 0, 0, true, true>(sms, "hybrid_13tt_3bs");
+        run<3, 1, 0, 0, true, true>(sms, "hybrid_15tt_1bs");
+        run<3, 2, 0, 0, false, true>(sms, "hybrid_2bs");
+        return 0;
+    }
     run<4, 0, 0, 0>(sms, "ttable_16w");
     run<3, 0, 0, 0>(sms, "ttable_12w");
     run<0, 4, 0, 0>(sms, "bitsliced_4w_alone");
@@ -201,5 +355,9 @@ int main() {
     run<3, 1, 0, 0, true>(sms, "hybrid_15tt_1bs");
     run<3, 3, 0, 0, true>(sms, "hybrid_13tt_3bs");
     run<3, 2, 64, 0, true>(sms, "hybrid_14tt_2bs_sleep");
+    run<3, 2, 0, 0, true, true>(sms, "hybrid_14tt_2bs");
+    run<3, 3, 0, 0, true, true>(sms, "hybrid_13tt_3bs");
+    run<3, 1, 0, 0, true, true>(sms, "hybrid_15tt_1bs");
+    run<3, 2, 0, 0, false, true>(sms, "hybrid_2bs");
     return 0;
 }
