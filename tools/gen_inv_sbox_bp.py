@@ -20,8 +20,11 @@ common-subexpression heuristic.  The circuit is evaluated on all 256 inputs
 against the inverse S-box computed here from its definition before anything
 is written.  Tool code: not the product library, not the oracle.
 
-usage: python tools/gen_inv_sbox_bp.py > tools/kg_inv_sbox_bp.cuh
+usage: python tools/gen_inv_sbox_bp.py [OUT.cuh]   (default: stdout, named kg_inv_sbox_bp.cuh)
+  tools/kg_inv_sbox_bp.cuh               -- the hybrid microbenchmark's copy
+  paper_1305_3345_b200/csrc/kg_bs_inv_sbox.cuh -- the product's (kg_hybrid kernel)
 """
+import os
 import sys
 
 sys.path.insert(0, __import__("os").path.dirname(__file__))
@@ -173,7 +176,9 @@ def main():
         sys.exit(f"inverse circuit wrong on {len(bad)} inputs, first {bad[0]:#04x}")
     gates = sum(max(1, l.count("^") + l.count("&")) for l in circuit if "=" in l)
     n_and = sum(l.count("&") for l in circuit)
-    out = ["// kg_inv_sbox_bp.cuh -- GENERATED by tools/gen_inv_sbox_bp.py; do not edit.",
+    path = sys.argv[1] if len(sys.argv) > 1 else None
+    fname = os.path.basename(path) if path else "kg_inv_sbox_bp.cuh"
+    out = [f"// {fname} -- GENERATED by tools/gen_inv_sbox_bp.py; do not edit.",
            "// AES inverse S-box, bitsliced on 32 blocks per word: affine top layer (Paar XOR network),",
            "// the Boyar-Peralta nonlinear core (%d AND), linear bottom layer (Paar); ~%d two-input" % (n_and, gates),
            "// gates; verified on all 256 inputs at generation time.",
@@ -188,7 +193,12 @@ def main():
     for i in range(8):
         out.append(f"    x[{7 - i}] = O{i};")
     out.append("}")
-    print("\n".join(out))
+    text = "\n".join(out) + "\n"
+    if path:
+        with open(path, "w") as f:
+            f.write(text)
+    else:
+        sys.stdout.write(text)
     print(f"inverse S-box circuit: {gates} gates ({n_and} AND), top {len(top_lines)} shared XOR, "
           f"bottom {len(bot_lines)} shared XOR; verified on 256 inputs", file=sys.stderr)
 
