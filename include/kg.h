@@ -171,7 +171,6 @@ KG_API const char *kg_strerror(int status);
  *   KG_RAMP_WARM=0   treat every staged batch as cold (ramps, 8 MiB auto chunks)
  *   KG_KEYED=0|1     mixed-key kernels: one block per lane / __ldg round keys
  *   KG_PAIR=0        one block per lane instead of block pairs
- *   KG_HYBRID=0      no hybrid (T-table + bitsliced) decryption kernel
  *   KG_PDL=0         no programmatic dependent launch
  *   KG_TRACE=1       per-chunk staging timeline on stderr at kg_wait
  *   KG_NSK_STAMPS=1  NSK per-request %globaltimer stamps;  KG_DEBUG=1 CUDA errors */
@@ -282,12 +281,6 @@ KG_API int kg_free_pinned(void *p);
 /* Number of CUDA kernels this library has launched in this process
  * (instrumentation for benchmarks; monotonic, never reset). */
 KG_API uint64_t kg_launch_count(void);
-
-/* Of those, the launches of the hybrid decryption kernel (T-table warps +
- * bitsliced warps): large device-input CBC/ECB decryption
- * batches of power-of-two pages of 32 B .. 16 KiB (KG_HYBRID=0: never).
- * Instrumentation; monotonic, never reset. */
-KG_API uint64_t kg_hybrid_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ MAX_INFLIGHT = 65536
 
 #: every symbol include/kg.h declares
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",
-               "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_hybrid_launch_count", "kg_set_host_path",
+               "kg_strerror", "kg_set_pipeline", "kg_launch_count", "kg_set_host_path",
                "kg_nsk_start", "kg_nsk_stop", "kg_nsk_dispatch", "kg_alloc_pinned", "kg_free_pinned",
                "kg_submit_pages_keyed", "kg_dispatch_threshold", "kg_nsk_calibration")
 NSK_DIRECT, NSK_NOCAL = 1, 2
@@ -81,8 +81,6 @@ _lib.kg_nsk_calibration.argtypes = [ctypes.POINTER(CalibPoint), ctypes.c_int]
 _lib.kg_nsk_calibration.restype = ctypes.c_int
 _lib.kg_launch_count.argtypes = []
 _lib.kg_launch_count.restype = ctypes.c_uint64
-_lib.kg_hybrid_launch_count.argtypes = []
-_lib.kg_hybrid_launch_count.restype = ctypes.c_uint64
 
 
 class KgError(RuntimeError):
@@ -231,10 +229,6 @@ def free_pinned(t) -> None:
 
 def launch_count() -> int:
     return int(_lib.kg_launch_count())
-
-
-def hybrid_launch_count() -> int:
-    return int(_lib.kg_hybrid_launch_count())
 
 
 def crypt_pages(direction: int, mode: int, inp, out, n_pages: int, page_bytes: int, ivs, key_id: int,

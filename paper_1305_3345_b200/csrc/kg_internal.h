@@ -118,8 +118,6 @@ int expand_key(const uint8_t *key, int key_bytes, RoundKeys *enc, RoundKeys *dec
 cudaError_t kernels_init(const BaseTables &t);
 // Enqueue one batch on `st`.  dir/mode/nr validated by the caller.
 cudaError_t launch_pages(int dir, int mode, int nr, const LaunchArgs &a, int num_sms, cudaStream_t st);
-// Launches of the hybrid decryption kernel so far (kg_hybrid_launch_count).
-uint64_t hybrid_launches();
 // Mixed-key batch: page p uses key k.key_ids[p] (all of size nr).
 cudaError_t launch_pages_keyed(int dir, int mode, int nr, const LaunchArgs &a, const KeyedArgs &k, int num_sms,
                                cudaStream_t st);

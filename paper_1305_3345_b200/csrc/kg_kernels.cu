@@ -39,10 +39,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
-#include <atomic>
-
 #include "kg_internal.h"
-#include "kg_bitslice.cuh"
 
 namespace kg {
 
@@ -400,14 +397,11 @@ __device__ __forceinline__ void ld_group(const Job &a, uint64_t q, uint4 (&x)[G]
 
 // Stream the groups [w0, w1) of one warp.  nx holds the warp's first unit
 // (already loaded); carry = C of the block before w0 (if not a page start).
-// progress != nullptr (the hybrid kernel): lane 0 adds each unit's groups to it.
 template <int G, bool DEC, bool CBC, bool TEX, class Cipher>
 __device__ __forceinline__ void group_stream(const Job &a, const Cipher &cph, uint64_t w0, uint64_t w1, uint64_t mg,
-                                             uint4 carry, uint64_t page, uint32_t jg, uint4 (&nx)[G],
-                                             unsigned long long *progress = nullptr) {
+                                             uint4 carry, uint64_t page, uint32_t jg, uint4 (&nx)[G]) {
     const uint32_t lane = threadIdx.x & 31;
     for (uint64_t u = w0; u < w1; u += 32) {
-        if (progress && lane == 0) atomicAdd(progress, (unsigned long long)(w1 - u < 32 ? w1 - u : 32));
         const uint64_t q = u + lane;
         const bool act = q < w1;
         uint4 x[G];
@@ -651,203 +645,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) kg_cbc_enc(const __grid_cons
         st[2] = t_waited;
     }
 #endif
-}
-
-// ---- hybrid decryption: T-table warps + bitsliced warps ----------------------
-// The T-table round saturates the shared-memory data path (the lookups) while
-// leaving ~25% of the ALU pipe idle; bitsliced AES (kg_bitslice.cuh) is pure
-// LOP3.  One 512-thread CTA per SM: 14 warps run the block-pair T-table body,
-// warps 12 and 13 (warpgroup 3, on two of the four SM sub-partitions) run the
-// bitsliced inverse cipher on units of 1,024 blocks (32 lanes x 32 blocks).
-// Measured in isolation: 2.12 block-rounds/clk/SM against 1.99 for T-table
-// warps alone (profiles/r2_bitslice).  `setmaxnreg` moves registers from the
-// T-table warpgroups (88 each) to warpgroup 3 (232: 128 state words).
-//
-// Work split inside a CTA (whole pages: CTA ranges, bitsliced units and, in
-// place, the T-table pool claims): the T-table warps split the first
-// (1 - 1/KG_HYB_POOL_DIV) of the CTA's pages statically; the rest is a pool
-// the T-table warps drain from the bottom (as kg_blockpar's tail pool) and the
-// bitsliced warps from the top, one unit at a time, through one 64-bit shared
-// word (hi << 32 | lo).  A bitsliced warp only claims a unit while the
-// T-table warps have at least kHybRminPairs pairs left: a unit takes a
-// bitsliced warp about as long as the T-table warps need for ~14K pairs, and
-// the CTA must not wait for a late unit.
-#ifndef KG_HYB_POOL_DIV
-#define KG_HYB_POOL_DIV 6
-#endif
-constexpr int kHybThreads = 512;
-constexpr int kHybBsWarp0 = 12, kHybBsWarps = 2;   // warps 12, 13 of warpgroup 3
-constexpr uint32_t kHybUnitPairs = 512;            // 1,024 blocks
-constexpr uint64_t kHybRminPairs = 16384;
-// runtime copy of the claim threshold (KG_HYB_RMIN, pairs; A/B experiments)
-__constant__ unsigned long long c_hyb_rmin = kHybRminPairs;
-constexpr int kSmemHyb = kSmemDec + 15 * 128 * 4;   // + bitsliced round-key masks
-
-struct HybPool {
-    unsigned long long pool;     // (hi << 32) | lo: pool pairs [cmid + lo, cmid + hi) unclaimed
-    unsigned long long tt_done;  // pairs finished by the T-table warps
-    unsigned long long bs_taken; // pairs claimed by the bitsliced warps
-};
-
-// {02}/{03} column mix of one little-endian word (FIPS-197 §5.1.3): used to
-// recover w[] from the equivalent-inverse schedule (§5.3.5) in LaunchArgs.
-__device__ __forceinline__ uint32_t hyb_gm2(uint32_t x) {
-    return ((x & 0x7f7f7f7fu) << 1) ^ (((x >> 7) & 0x01010101u) * 0x1bu);
-}
-__device__ __forceinline__ uint32_t hyb_mix_word(uint32_t x) {
-    const uint32_t r1 = __funnelshift_r(x, x, 8), r2 = __funnelshift_r(x, x, 16), r3 = __funnelshift_r(x, x, 24);
-    return hyb_gm2(x) ^ hyb_gm2(r1) ^ r1 ^ r2 ^ r3;  // out_r = 2 a_r ^ 3 a_{r+1} ^ a_{r+2} ^ a_{r+3}
-}
-
-// One bitsliced unit: the 1,024 blocks [b0, b0 + 1024), lane l holding blocks
-// b0 + 32k + l (k = 0..31, coalesced loads and stores).
-template <int NR, bool CBC>
-__device__ __forceinline__ void hyb_bs_unit(const Job &a, uint64_t b0, const uint4 (*msk)[32], uint32_t log2m) {
-    const uint32_t lane = threadIdx.x & 31;
-    uint32_t s[128];
-#pragma unroll
-    for (int k = 0; k < 32; k++) {
-        const uint4 x = tex1Dfetch<uint4>((cudaTextureObject_t)a.tex, (int)(a.tex_off + (int64_t)(b0 + 32 * k + lane)));
-        s[k] = x.x;
-        s[32 + k] = x.y;
-        s[64 + k] = x.z;
-        s[96 + k] = x.w;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; c++) bs::transpose32(s + 32 * c);
-    bs::inv_cipher<NR>(s, msk);
-#pragma unroll
-    for (int c = 0; c < 4; c++) bs::transpose32(s + 32 * c);
-    const uint64_t mmask = (1ull << log2m) - 1;
-    // Descending slots: the predecessor of slot k's block is slot k's block of
-    // the previous lane or, for lane 0, slot k-1's block of lane 31 -- in
-    // place, neither may have been stored yet when it is fetched.
-#pragma unroll
-    for (int k = 31; k >= 0; k--) {
-        const uint64_t b = b0 + 32 * k + lane;
-        uint4 o = make_uint4(s[k], s[32 + k], s[64 + k], s[96 + k]);
-        if (CBC) {
-            const uint4 p = (b & mmask) == 0 ? a.ivs[b >> log2m]
-                                             : tex1Dfetch<uint4>((cudaTextureObject_t)a.tex, (int)(a.tex_off + (int64_t)(b - 1)));
-            o = xor4(o, p);
-        }
-        st_stream(a.out + b, o);
-    }
-}
-
-// T-table warps: the static share [w0, w1) (first unit already in nx), then
-// pool claims from the bottom; progress published in hp.tt_done.
-template <int NR, bool CBC>
-__device__ __forceinline__ void hyb_tt_role(const Job &a, const RoundKeys &rk, const char *sm, HybPool &hp, uint64_t w0,
-                                            uint64_t w1, uint64_t mg, uint64_t cmid, uint4 carry, uint4 (&nx)[2]) {
-    const uint32_t lane = threadIdx.x & 31;
-    const ParamDec<NR> cph{sm, lane_bytes(), rk};
-    const uint64_t page = (w0 + lane) / mg;
-    const uint32_t jg = (uint32_t)((w0 + lane) - page * mg);
-    group_stream<2, true, CBC, true>(a, cph, w0, w1, mg, carry, page, jg, nx, &hp.tt_done);
-    const uint64_t unit = a.in_place ? mg : 32;
-    for (;;) {
-        unsigned long long old = 0;
-        if (lane == 0) old = atomicAdd(&hp.pool, (unsigned long long)unit);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        const uint64_t lo = old & 0xffffffffull, hi = old >> 32;
-        if (lo >= hi) break;
-        const uint64_t q0 = cmid + lo, q1 = cmid + (lo + unit < hi ? lo + unit : hi);
-        const uint64_t pg = (q0 + lane) / mg;
-        const uint32_t jl = (uint32_t)(q0 + lane - pg * mg);
-        if (q0 + lane < q1) ld_group<2, true>(a, q0 + lane, nx);
-        uint4 cr = make_uint4(0, 0, 0, 0);
-        if (CBC && q0 % mg != 0) cr = a.in[2 * q0 - 1];  // out of place only (in place: q0 is a page start)
-        group_stream<2, true, CBC, true>(a, cph, q0, q1, mg, cr, pg, jl, nx, &hp.tt_done);
-    }
-}
-
-// Bitsliced warps: claim units from the top of the pool while the T-table
-// warps have enough work left to cover one unit (see above).
-template <int NR, bool CBC>
-__device__ __forceinline__ void hyb_bs_role(const Job &a, HybPool &hp, const uint4 (*msk)[32], uint64_t c0, uint64_t c1,
-                                            uint64_t cmid) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t log2m = 31 - __clz(a.m);
-    for (;;) {
-        unsigned long long got = ~0ull;
-        if (lane == 0) {
-            for (;;) {
-                const unsigned long long old = *reinterpret_cast<volatile unsigned long long *>(&hp.pool);
-                const uint64_t lo = old & 0xffffffffull, hi = old >> 32;
-                if (hi < lo + kHybUnitPairs) break;
-                const uint64_t done = *reinterpret_cast<volatile unsigned long long *>(&hp.tt_done);
-                const uint64_t taken = *reinterpret_cast<volatile unsigned long long *>(&hp.bs_taken);
-                const uint64_t t_left = (c1 - c0) - taken - done;
-                if (t_left < kHybUnitPairs + c_hyb_rmin) break;
-                if (atomicCAS(&hp.pool, old, old - ((unsigned long long)kHybUnitPairs << 32)) == old) {
-                    atomicAdd(&hp.bs_taken, (unsigned long long)kHybUnitPairs);
-                    got = cmid + hi - kHybUnitPairs;
-                    break;
-                }
-            }
-        }
-        got = __shfl_sync(0xffffffffu, got, 0);
-        if (got == ~0ull) break;
-        hyb_bs_unit<NR, CBC>(a, 2 * got, msk, log2m);
-    }
-}
-
-template <int NR, int MODE>
-__global__ void __launch_bounds__(kHybThreads, 1) kg_hybrid(const __grid_constant__ LaunchArgs la) {
-    extern __shared__ __align__(16) char sm[];
-    constexpr bool CBC = (MODE == 0);
-    __shared__ HybPool hp;
-    const Job a = job_of(la);
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool bs_warp = warp >= (uint32_t)kHybBsWarp0 && warp < (uint32_t)(kHybBsWarp0 + kHybBsWarps);
-    uint4(*msk)[32] = reinterpret_cast<uint4(*)[32]>(sm + kSmemDec);
-    fill_tables<true>(sm);
-    // bitsliced round-key masks: InvCipher round key j = w[4j .. 4j+3] of the
-    // encryption schedule; LaunchArgs holds the equivalent-inverse schedule
-    // dk[r] (dk[0] = w[Nr], dk[Nr] = w[0], else InvMixColumns(w[Nr - r])).
-    for (int e = threadIdx.x; e < (NR + 1) * 128; e += blockDim.x) {
-        const int j = e >> 7, p = e & 127, c = p >> 5, bit = p & 31;
-        uint32_t w = la.rk.w[4 * (NR - j) + c];
-        if (j != 0 && j != NR) w = hyb_mix_word(w);
-        reinterpret_cast<uint32_t *>(msk[j])[p] = 0u - ((w >> bit) & 1u);
-    }
-    const uint64_t mg = a.m / 2;  // pairs per page
-    const uint64_t P0 = part_start(a.n_pages, gridDim.x, blockIdx.x), P1 = part_start(a.n_pages, gridDim.x, blockIdx.x + 1);
-    const uint64_t c0 = P0 * mg, c1 = P1 * mg;
-    const uint64_t cmid = (P1 - (P1 - P0) / KG_HYB_POOL_DIV) * mg;
-    if (threadIdx.x == 0) {
-        hp.pool = (unsigned long long)(c1 - cmid) << 32;
-        hp.tt_done = 0;
-        hp.bs_taken = 0;
-    }
-    pdl_prologue_done();
-    // T-table warps: static share of [c0, cmid) over 14 warps, first unit in flight
-    const uint32_t tw = warp < (uint32_t)kHybBsWarp0 ? warp : warp - kHybBsWarps;
-    constexpr uint32_t kTw = kHybThreads / 32 - kHybBsWarps;
-    uint64_t w0 = 0, w1 = 0;
-    uint4 carry = make_uint4(0, 0, 0, 0);
-    uint4 nx[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-    if (!bs_warp) {
-        small_split(c0, cmid, tw, kTw, w0, w1);
-        if (CBC && w0 < w1 && (w0 % mg) != 0) carry = a.in[2 * w0 - 1];
-        if (w0 + lane < w1) ld_group<2, true>(a, w0 + lane, nx);
-    }
-    __syncthreads();  // in place: every snapshot above happens before any store
-    // The bitsliced code sits under the setmaxnreg.inc that sizes it (232
-    // registers); the T-table code is reached from both branches, so ptxas
-    // sizes it for 88 -- and it exists once: two copies of the ~18 KB T-table
-    // loop running at once overflow the instruction cache (profiles/r2_hybrid).
-    if (warp >= 12) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-        if (bs_warp) {
-            hyb_bs_role<NR, CBC>(a, hp, msk, c0, c1, cmid);
-            return;
-        }
-    } else {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
-    }
-    hyb_tt_role<NR, CBC>(a, la.rk, sm, hp, w0, w1, mg, cmid, carry, nx);
 }
 
 // ---- mixed-key batches -------------------------------------------------------
@@ -1136,8 +933,6 @@ cudaError_t init_nr() {
     if ((e = set_smem(kg_keyed_pair<NR, 1, 0, false>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_pair<NR, 1, 1, false>, kSmemDec)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_pair<NR, 0, 1, false>, kSmemEnc)) != cudaSuccess) return e;
-    if ((e = set_smem(kg_hybrid<NR, 0>, kSmemHyb)) != cudaSuccess) return e;
-    if ((e = set_smem(kg_hybrid<NR, 1>, kSmemHyb)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_chain<NR, true>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_chain<NR, false>, kSmemEnc)) != cudaSuccess) return e;
     if ((e = set_smem(kg_keyed_chain<NR, true, true>, kSmemEnc)) != cudaSuccess) return e;
@@ -1170,22 +965,6 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, int smem, cudaSt
     return launch_pdl_tpb(kernel, grid, kThreads, smem, st, args...);
 }
 
-// The hybrid kernel (decryption, texture-pipe loads, block pairs): pages of a
-// power-of-two number of blocks up to 1,024 (so a bitsliced unit is whole
-// pages) and CTA ranges long enough for the bitsliced warps to finish units
-// well before the T-table warps (>= 2 x kHybRminPairs pairs per CTA: 256
-// pages of 4 KiB).  KG_HYBRID=0: block-pair kernel only (A/B).
-std::atomic<uint64_t> g_hybrid_launches{0};
-
-bool hybrid_ok(const LaunchArgs &a, unsigned grid) {
-    static const int on = [] {
-        const char *e = getenv("KG_HYBRID");
-        return (e && *e == '0') ? 0 : 1;
-    }();
-    if (!on || a.m < 2 || a.m > 1024 || (a.m & (a.m - 1)) != 0 || a.host_io) return false;
-    return a.n_pages / grid * (a.m / 2) >= 2 * kHybRminPairs;
-}
-
 template <int NR>
 cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaStream_t st) {
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
@@ -1210,11 +989,6 @@ cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaS
         return (e && *e == '0') ? 0 : 1;
     }();
     const bool wide = pair_ok && wide_ok(a.m, a.in, a.out);
-    if (wide && a.tex_in && dir == 1 && hybrid_ok(a, grid)) {
-        g_hybrid_launches.fetch_add(1, std::memory_order_relaxed);
-        if (mode == 0) return launch_pdl_tpb(kg_hybrid<NR, 0>, grid, kHybThreads, kSmemHyb, st, a);
-        return launch_pdl_tpb(kg_hybrid<NR, 1>, grid, kHybThreads, kSmemHyb, st, a);
-    }
     if (wide && a.tex_in) {
         if (dir == 1 && mode == 0) return launch_pdl_tpb(kg_blockpar<NR, 1, 0, true, true>, grid, kPairThreads, kSmemDec, st, a);
         if (dir == 1) return launch_pdl_tpb(kg_blockpar<NR, 1, 1, true, true>, grid, kPairThreads, kSmemDec, st, a);
@@ -1310,16 +1084,10 @@ cudaError_t kernels_init(const BaseTables &t) {
     cudaError_t e = cudaMemcpyToSymbol(g_tables, &t, sizeof(BaseTables));
     if (e != cudaSuccess) return e;
     if ((e = set_smem(kg_nsk, kSmemNsk)) != cudaSuccess) return e;
-    if (const char *r = getenv("KG_HYB_RMIN")) {
-        const unsigned long long v = strtoull(r, nullptr, 0);
-        if ((e = cudaMemcpyToSymbol(c_hyb_rmin, &v, sizeof v)) != cudaSuccess) return e;
-    }
     if ((e = init_nr<10>()) != cudaSuccess) return e;
     if ((e = init_nr<12>()) != cudaSuccess) return e;
     return init_nr<14>();
 }
-
-uint64_t hybrid_launches() { return g_hybrid_launches.load(); }
 
 cudaError_t launch_pages(int dir, int mode, int nr, const LaunchArgs &a, int num_sms, cudaStream_t st) {
     switch (nr) {

@@ -881,8 +881,6 @@ const char *kg_strerror(int status) {
 
 uint64_t kg_launch_count(void) { return g_launches.load(); }
 
-uint64_t kg_hybrid_launch_count(void) { return kg::hybrid_launches(); }
-
 int kg_init(int device) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (g.up) return device == g.device ? KG_OK : KG_EINVAL;

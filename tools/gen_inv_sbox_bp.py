@@ -21,8 +21,8 @@ against the inverse S-box computed here from its definition before anything
 is written.  Tool code: not the product library, not the oracle.
 
 usage: python tools/gen_inv_sbox_bp.py [OUT.cuh]   (default: stdout, named kg_inv_sbox_bp.cuh)
-  tools/kg_inv_sbox_bp.cuh               -- the hybrid microbenchmark's copy
-  paper_1305_3345_b200/csrc/kg_bs_inv_sbox.cuh -- the product's (kg_hybrid kernel)
+  tools/kg_inv_sbox_bp.cuh -- the hybrid microbenchmark's copy (the product kernel that used
+  it, kg_hybrid, is in git history: profiles/r2_hybrid)
 """
 import os
 import sys
