@@ -607,6 +607,9 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
         st[0] = t_start;
         st[1] = t_filled;
         st[2] = t_waited;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        st[kStampW - 1] = smid;
     }
 #endif
 }
@@ -643,6 +646,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) kg_cbc_enc(const __grid_cons
         st[0] = t_start;
         st[1] = t_filled;
         st[2] = t_waited;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        st[kStampW - 1] = smid;
     }
 #endif
 }

@@ -110,6 +110,23 @@ int main(int argc, char **argv) {
         prev_first_wait = first_wait;
     }
     printf("]}\n");
+    // per-CTA rows of the last launch: SM id, start, first and last warp done (us from its first start)
+    if (getenv("KG_STAMPS_PER_CTA")) {
+        auto &L = h[order.back()];
+        unsigned long long s0 = ~0ull;
+        for (int c = 0; c < 148; c++) s0 = std::min(s0, L[c][0]);
+        printf("{\"per_cta_last_launch\": [");
+        for (int c = 0; c < 148; c++) {
+            unsigned long long dmin = ~0ull, dmax = 0;
+            for (int w = 0; w < warps; w++) {
+                dmin = std::min(dmin, L[c][3 + w]);
+                dmax = std::max(dmax, L[c][3 + w]);
+            }
+            printf("%s[%d, %llu, %.2f, %.2f, %.2f]", c ? ", " : "", c, L[c][kg::kStampW - 1], (L[c][0] - s0) * 1e-3,
+                   (dmin - s0) * 1e-3, (dmax - s0) * 1e-3);
+        }
+        printf("]}\n");
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e));
     return 0;

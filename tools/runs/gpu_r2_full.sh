@@ -2,7 +2,7 @@
 # round-2 end-to-end check on one B200: the GPU test suite, smoke(), the default
 # bench line exactly as the driver runs it, the reference arm, the bench's ncu
 # launch list, and an NVTX-filtered ncu capture (the kgpu ranges exist).
-OUT=gpurun_out/r2_full
+OUT=gpurun_out/${1:-r2_full}
 mkdir -p $OUT
 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=25 > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest.log
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
