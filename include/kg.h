@@ -171,6 +171,7 @@ KG_API const char *kg_strerror(int status);
  *   KG_RAMP_WARM=0   treat every staged batch as cold (ramps, 8 MiB auto chunks)
  *   KG_KEYED=0|1     mixed-key kernels: one block per lane / __ldg round keys
  *   KG_PAIR=0        one block per lane instead of block pairs
+ *   KG_CHAIN_ALIGN=n CBC-encrypt CTA page ranges start at multiples of n pages (default 4)
  *   KG_PDL=0         no programmatic dependent launch
  *   KG_TRACE=1       per-chunk staging timeline on stderr at kg_wait
  *   KG_NSK_STAMPS=1  NSK per-request %globaltimer stamps;  KG_DEBUG=1 CUDA errors */

@@ -54,6 +54,16 @@ constexpr int kSmemEnc = 2 * kRegion;                       // Te0..Te3
 constexpr int kSmemDec = 2 * kRegion + 255 * 256 + 128;     // Td0..Td3 + Si (t = 0 slots only)
 
 __device__ BaseTables g_tables;
+// CBC-encrypt chain kernels: CTA page ranges start at multiples of this many
+// pages.  A warp's 32 lanes walk 32 consecutive pages 4 KiB apart; with CTA
+// ranges starting at an odd page or 2 mod 4 those CTAs ran 2% slower (~1,752
+// vs ~1,708 us per C3 launch, bimodal by the range's start), and the launch
+// waited for them: aligned to 4 pages C3 goes 604 -> 617 GB/s and the CTAs'
+// finishing spread 42 -> 5 us (profiles/r2_chain_align).  KG_CHAIN_ALIGN
+// overrides it (A/B).
+constexpr unsigned long long kChainAlign = 4;
+__constant__ unsigned long long c_chain_align = kChainAlign;
+unsigned long long g_chain_align = kChainAlign;  // host copy (grid sizing)
 #ifdef KG_CTA_STAMPS
 // diagnostics build (tools/cta_stamps.cu): %globaltimer per CTA of the last 8
 // launches: [0] start, [1] tables filled, [2] griddepcontrol.wait returned,
@@ -512,8 +522,12 @@ __device__ __forceinline__ void blockpair_body(const Job &a, const Cipher &cph, 
 template <bool WIDE, class Cipher, bool TEX = false>
 __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, uint32_t cta, uint32_t ncta) {
     const uint32_t m = a.m;
-    const uint64_t p0 = part_start(a.n_pages, ncta, cta);
-    const uint64_t p1 = part_start(a.n_pages, ncta, cta + 1);
+    // CTA page ranges start at multiples of c_chain_align pages (see kChainAlign)
+    const uint64_t A = c_chain_align;
+    const uint64_t nu = (a.n_pages + A - 1) / A;
+    uint64_t p0 = part_start(nu, ncta, cta) * A, p1 = part_start(nu, ncta, cta + 1) * A;
+    if (p0 > a.n_pages) p0 = a.n_pages;
+    if (p1 > a.n_pages) p1 = a.n_pages;
     for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const uint4 *src = a.in + p * m;
         uint4 *dst = a.out + p * m;
@@ -975,7 +989,8 @@ template <int NR>
 cudaError_t launch_nr(int dir, int mode, const LaunchArgs &a, int num_sms, cudaStream_t st) {
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     if (dir == 0 && mode == 0) {
-        const unsigned grid = (unsigned)(a.n_pages < (uint64_t)num_sms ? a.n_pages : (uint64_t)num_sms);
+        const uint64_t units = (a.n_pages + g_chain_align - 1) / g_chain_align;  // CTA ranges of whole units
+        const unsigned grid = (unsigned)(units < (uint64_t)num_sms ? units : (uint64_t)num_sms);
         const bool wide = wide_ok(a.m, a.in, a.out);
         if (wide && a.tex_in)
             return launch_pdl_tpb(kg_cbc_enc<NR, true, true>, grid, kChainThreads, kSmemEnc, st, a);
@@ -1025,7 +1040,7 @@ template <int NR>
 cudaError_t launch_keyed_nr(int dir, int mode, const LaunchArgs &a, const KeyedArgs &k, int num_sms, cudaStream_t st) {
     const uint64_t nb = a.n_pages * (uint64_t)a.m;
     const bool chain = (dir == 0 && mode == 0);
-    uint64_t want = chain ? a.n_pages : a.host_io ? (nb + 255) / 256 : (nb + 63) / 64;
+    uint64_t want = chain ? (a.n_pages + g_chain_align - 1) / g_chain_align : a.host_io ? (nb + 255) / 256 : (nb + 63) / 64;
     if (want > (uint64_t)num_sms) want = (uint64_t)num_sms;
     if (a.in_place && want > a.n_pages) want = a.n_pages;
     if (want < 1) want = 1;
@@ -1090,6 +1105,13 @@ cudaError_t kernels_init(const BaseTables &t) {
     cudaError_t e = cudaMemcpyToSymbol(g_tables, &t, sizeof(BaseTables));
     if (e != cudaSuccess) return e;
     if ((e = set_smem(kg_nsk, kSmemNsk)) != cudaSuccess) return e;
+    if (const char *r = getenv("KG_CHAIN_ALIGN")) {
+        const unsigned long long v = strtoull(r, nullptr, 0);
+        if (v >= 1) {
+            if ((e = cudaMemcpyToSymbol(c_chain_align, &v, sizeof v)) != cudaSuccess) return e;
+            g_chain_align = v;
+        }
+    }
     if ((e = init_nr<10>()) != cudaSuccess) return e;
     if ((e = init_nr<12>()) != cudaSuccess) return e;
     return init_nr<14>();
