@@ -61,7 +61,15 @@ int main(int argc, char **argv) {
     cudaEventCreate(&ev0);
     cudaEventCreate(&ev1);
     cudaEventRecord(ev0, st);
-    for (int rep = 0; rep < nl; rep++) kg::launch_pages(enc ? 0 : 1, 0, enc ? 14 : 10, a, 148, st);
+    // KG_STAMPS_EVENTS=1: an event record after every launch, as the runtime's
+    // per-ticket completion events do (does it break the PDL overlap?)
+    const bool with_events = getenv("KG_STAMPS_EVENTS") != nullptr;
+    std::vector<cudaEvent_t> evs(nl);
+    for (auto &e : evs) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (int rep = 0; rep < nl; rep++) {
+        kg::launch_pages(enc ? 0 : 1, 0, enc ? 14 : 10, a, 148, st);
+        if (with_events) cudaEventRecord(evs[rep], st);
+    }
     cudaEventRecord(ev1, st);
     cudaStreamSynchronize(st);
     float ms = 0;
