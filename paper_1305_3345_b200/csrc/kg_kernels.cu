@@ -68,7 +68,7 @@ unsigned long long g_chain_align = kChainAlign;  // host copy (grid sizing)
 // diagnostics build (tools/cta_stamps.cu): %globaltimer per CTA of the last 8
 // launches: [0] start, [1] tables filled, [2] griddepcontrol.wait returned,
 // [3 + w] warp w done (<= 32 warps)
-constexpr int kStampW = 36;
+constexpr int kStampW = 38;  // + [35] clock64 at the wait release, [36] clock64 at the end (thread 0), [37] %smid
 __device__ unsigned long long g_stamps[8][148][kStampW];
 __device__ unsigned int g_stamp_ctr;
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
     pdl_prologue_done();
 #ifdef KG_CTA_STAMPS
     const unsigned long long t_waited = gtimer();
+    const unsigned long long c_waited = clock64();
 #endif
     const uint32_t lb = lane_bytes();
     if (PAIR) {
@@ -624,6 +625,8 @@ __global__ void __launch_bounds__(PAIR ? kPairThreads : kThreads, 1) kg_blockpar
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         st[kStampW - 1] = smid;
+        st[kStampW - 3] = c_waited;
+        st[kStampW - 2] = clock64();
     }
 #endif
 }
@@ -650,6 +653,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) kg_cbc_enc(const __grid_cons
     __syncthreads();
 #ifdef KG_CTA_STAMPS
     const unsigned long long t_waited = gtimer();
+    const unsigned long long c_waited = clock64();
 #endif
     cbc_enc_body<WIDE, ParamEnc<NR>, TEX>(job_of(a), ParamEnc<NR>{sm, lane_bytes(), a.rk}, blockIdx.x, gridDim.x);
 #ifdef KG_CTA_STAMPS
@@ -663,6 +667,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) kg_cbc_enc(const __grid_cons
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         st[kStampW - 1] = smid;
+        st[kStampW - 3] = c_waited;
+        st[kStampW - 2] = clock64();
     }
 #endif
 }
