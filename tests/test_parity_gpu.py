@@ -337,3 +337,16 @@ def test_staged_device_input_one_batch_texture(direction, mode):
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
     torch.cuda.synchronize()
     assert first_mismatch(out.numpy(), exp) is None
+
+
+@pytest.mark.parametrize("n", [4, 7, 591, 592, 593, 595, 599, 1183, 4733])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_cbc_encrypt_chain_units(n, inplace):
+    """CBC-encrypt chain kernels deal pages to CTAs in 4-page units (kChainAlign):
+    batch sizes around 148 x 4 pages and odd remainders, every byte vs the oracle."""
+    key = synth.make_key(32, seed=900 + n)
+    data = synth.make_pages(n, 4096, seed=901 + n)
+    ivs = synth.make_ivs(n, seed=902 + n)
+    exp = oracle_pages(0, 0, key, data, n, 4096, ivs)
+    got = gpu_pages(0, 0, key, data, n, 4096, ivs, where="device", inplace=inplace)
+    assert first_mismatch(got, exp) is None
