@@ -766,6 +766,27 @@ def c4_sweep(ctx, args):
                         cb[p * PB:(p + 1) * PB])
             row["openssl_1core_us"] = round(lat(ossl, 5 if n < 256 else 2), 1)
         rows.append(row)
+    # Row f2: the size-based dispatcher as a caller sees it.  kg_nsk_start
+    # calibrates the NSK/launch crossover on the device (PAPER.md:493-495's
+    # "calibrate it using microbenchmarks at boot time"); requests up to the
+    # chosen size go to the resident kernel, larger ones are launched on the SMs
+    # it leaves free.
+    kg.nsk_start(16, kg.NSK_DIRECT, 5000)
+    try:
+        cal = kg.nsk_calibration()
+        dispatch = {"threshold_bytes": kg.dispatch_threshold(cal),
+                    "calibration": [{"bytes": b, "nsk_us": round(nu, 2), "launch_us": round(lu, 2)} for b, nu, lu in cal],
+                    "rule": "largest calibrated size below the first at which the launch is faster (tie -> NSK)"}
+        for row in rows:
+            n = row["pages"]
+
+            def g2():
+                kg.wait(kg.submit_pages(1, 0, dx, dout, n, PB, div, 0, s))
+            for _ in range(3):
+                g2()
+            row["auto_hbm_us"] = round(lat(g2, 50 if n * PB < (1 << 20) else 10), 2)
+    finally:
+        kg.nsk_stop()
     kg.free_pinned(hx)
     kg.free_pinned(hout)
     kg.free_pinned(hiv)
@@ -780,15 +801,16 @@ def c4_sweep(ctx, args):
         return {"bytes": None, "measured_pages": [pts[0]["pages"], pts[-1]["pages"]] if pts else None}
 
     cross = {}
-    for gk in ("hbm_us", "pinned_us", "nsk_hbm_us"):
+    for gk in ("hbm_us", "pinned_us", "nsk_hbm_us", "auto_hbm_us"):
         for ck in ("oracle_1t_us", "oracle_T_us", "openssl_1core_us"):
             cross[f"{gk[:-3]} vs {ck[:-3]}"] = crossover(gk, ck)
     return {"workload": "C4 request batch-size sweep: AES-128-CBC decrypt, one request of 2^k 4 KiB pages, "
                         f"k = 0..{kmax}; p50 latency in us (submit -> kg_wait returns, through Python), "
                         "p10/p90 and GB/s at the p50 for the launch paths",
-            "oracle_threads": threads, "rows": rows, "crossover": cross,
+            "oracle_threads": threads, "rows": rows, "crossover": cross, "nsk_dispatch": dispatch,
             "note": "crossover = smallest size from which the GPU p50 stays <= the CPU's (tie -> GPU); "
                     "openssl = single-core AES-NI via `cryptography`, context not the oracle; "
+                    "auto = the NSK running with its start-up calibrated dispatch (row f2); "
                     "the paper: GPU faster from 8 KB (PAPER.md:460-463)"}
 
 
