@@ -168,7 +168,8 @@ KG_API const char *kg_strerror(int status);
  *   KG_D2H_LAG=0|2|3 staged D2H not held back / only between equal chunks /
  *                    not for the last two chunks
  *   KG_RAMP_DOWN=0..3  end-ramp levels of a cold batch's staging schedule (default 3)
- *   KG_RAMP_WARM=0   treat every staged batch as cold (ramps, 8 MiB auto chunks)
+ *   KG_RAMP_WARM=0   treat every staged batch as cold (ramped auto chunks)
+ *   KG_CHUNK_WARM=n  auto chunk bytes of warm / >= 1 GiB staged batches (default 32 MiB)
  *   KG_KEYED=0|1     mixed-key kernels: one block per lane / __ldg round keys
  *   KG_PAIR=0        one block per lane instead of block pairs
  *   KG_CHAIN_ALIGN=n CBC-encrypt CTA page ranges start at multiples of n pages (default 4)
@@ -177,15 +178,15 @@ KG_API const char *kg_strerror(int status);
  *   KG_NSK_STAMPS=1  NSK per-request %globaltimer stamps;  KG_DEBUG=1 CUDA errors */
 
 /* Staging pipeline for batches touching host memory: chunk size in bytes
- * (rounded down to whole pages, at least one page; 0 = auto: 8 MiB with
- * ramped first/last chunks when the copy engines are idle at submit (16 MiB
- * for batches of 1 GiB or more), 16 MiB without ramps when earlier batches'
- * copies are still queued, and 16 MiB for
- * CBC encryption, whose per-page chains need the longer copy to hide behind)
- * and number of device staging slots (2..8).  Takes effect for
- * later submits.  Defaults: auto, 4 slots (PAPER.md:437-440's "three
- * buffers" plus one: the D2H of a chunk is held back until the next chunk's
- * H2D has landed, profiles/r1_lag).  Environment overrides at kg_init:
+ * (rounded down to whole pages, at least one page; 0 = auto: with the copy
+ * engines idle at submit, ramped first/last chunks of 8 MiB -- 16 MiB for
+ * CBC encryption, whose per-page chains need the longer copy to hide behind
+ * -- and 32 MiB for batches of 1 GiB or more; 32 MiB without ramps when
+ * earlier batches' copies are still queued) and number of device staging
+ * slots (2..8).  Takes effect for
+ * later submits.  Defaults: auto, 6 slots (PAPER.md:437-440's "three
+ * buffers", doubled: the D2H of a chunk is held back until the next chunk's
+ * H2D has landed, profiles/r1_lag, r2_e2e).  Environment overrides at kg_init:
  * KG_CHUNK_BYTES, KG_STAGING_SLOTS.  KG_EINVAL on bad values. */
 KG_API int kg_set_pipeline(uint64_t chunk_bytes, int slots);
 

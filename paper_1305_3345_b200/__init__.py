@@ -22,6 +22,7 @@ MODE_CBC, MODE_ECB = 0, 1
 OK, EINVAL, ENOKEY, ENOTINIT, EAGAIN, ENOMEM, ECUDA, ENOTSUP, ETICKET = 0, -1, -2, -3, -4, -5, -6, -7, -8
 MAX_KEYS = 256
 MAX_INFLIGHT = 65536
+DEFAULT_STAGING_SLOTS = 6  # kg_set_pipeline's default slot count (include/kg.h)
 
 #: every symbol include/kg.h declares
 ABI_SYMBOLS = ("kg_init", "kg_set_key", "kg_submit_pages", "kg_wait", "kg_poll", "kg_shutdown",

@@ -127,6 +127,7 @@ struct UseSet {
 };
 
 constexpr int kMaxSlots = 8;
+constexpr uint64_t kChunkWarm = 32ull << 20;  // staging chunk of warm / >= 1 GiB batches (submit_staged)
 constexpr int kKeySnaps = 4;
 constexpr uint32_t kStatusSlots = 1024;
 constexpr uint64_t kIvStageMax = 256ull << 20;  // IVs of up to 16M pages (64 GiB of 4 KiB pages)
@@ -142,13 +143,13 @@ struct Ctx {
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_begin = nullptr;
     Slot slots[kMaxSlots];
-    // 0 = auto: 8 MiB for block-parallel kernels (16 MiB when the pipeline is
-    // warm, submit_staged), 16 MiB for CBC-encrypt chains (whose per-chunk
-    // kernel is latency-bound at ~90 us below ~74 MiB, so it needs the longer
-    // copy to hide behind); measured with the lagged D2H,
+    // 0 = auto: 8 MiB for block-parallel kernels, 16 MiB for CBC-encrypt
+    // chains (whose per-chunk kernel is latency-bound at ~90 us below ~74 MiB,
+    // so it needs the longer copy to hide behind), 32 MiB when the pipeline is
+    // warm or the batch >= 1 GiB (submit_staged); measured with the lagged D2H,
     // profiles/r1_pinned/README.md, profiles/r2_e2e
     uint64_t chunk_bytes = 0;
-    int n_slots = 4;
+    int n_slots = 6;  // 6 x 32 MiB: profiles/r2_e2e (4 slots: -0.2 .. -0.4 GB/s)
     uint64_t slot_next = 0;    // slot of the next staged chunk (rotation continues across batches)
     uint64_t slot_bytes = 0;   // current allocation per slot (data)
     uint64_t slot_ivs = 0;     // current allocation per slot (ivs)
@@ -533,10 +534,10 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     // before this batch adds its own work).  A cold batch below 1 GiB is
     // bound by its fill and drain (small chunks and ramps, below); a warm or
     // a large one by the link, where fewer, larger copies win: auto chunk
-    // 8 MiB cold / 16 MiB warm or >= 1 GiB for the block-parallel kernels
-    // (C2 e2e 0.91 -> 0.95-0.97 of the duplex link with batches back to back;
-    // one 64 GiB C5 batch 0.96 -> 0.98; profiles/r2_e2e).  KG_RAMP_WARM=0:
-    // always cold.
+    // 8 MiB (16 MiB for CBC-encrypt chains) cold, 32 MiB warm or >= 1 GiB
+    // (C2 e2e with batches back to back 0.91 -> 0.97-0.98 of the duplex link,
+    // C4 at 1 GiB 0.99; profiles/r2_e2e).  KG_RAMP_WARM=0: always cold;
+    // KG_CHUNK_WARM: the warm/large chunk (A/B).
     static const bool warm_skip = [] {
         const char *e = getenv("KG_RAMP_WARM");
         return !(e && *e == '0');
@@ -546,10 +547,16 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
         warm = cudaStreamQuery(g.s_h2d) == cudaErrorNotReady;
         cudaGetLastError();
     }
-    const uint64_t cb = g.chunk_bytes ? g.chunk_bytes
-                        : (dir == KG_ENCRYPT && mode == KG_MODE_CBC) || warm || n_pages * page_bytes >= (1ull << 30)
-                            ? (16ull << 20)
-                            : (8ull << 20);
+    static const uint64_t big_chunk = [] {
+        const char *e = getenv("KG_CHUNK_WARM");
+        const unsigned long long v = e ? strtoull(e, nullptr, 0) : 0;
+        return v >= 16 ? (uint64_t)v : (uint64_t)kChunkWarm;
+    }();
+    const bool chain = (dir == KG_ENCRYPT && mode == KG_MODE_CBC);
+    const uint64_t cb = g.chunk_bytes                                     ? g.chunk_bytes
+                        : warm || n_pages * page_bytes >= (1ull << 30) ? big_chunk
+                        : chain                                         ? (16ull << 20)
+                                                                        : (8ull << 20);
     uint64_t chunk_pages = cb / page_bytes;
     if (chunk_pages < 1) chunk_pages = 1;
     if (chunk_pages > n_pages) chunk_pages = n_pages;
@@ -558,7 +565,7 @@ int submit_staged(int dir, int mode, int nr, const kg::RoundKeys &rk, const uint
     // so that a batch turning warm does not drain the pipeline to grow them
     uint64_t slot_pages = chunk_pages;
     if (!g.chunk_bytes) {
-        uint64_t wp = (16ull << 20) / page_bytes;
+        uint64_t wp = big_chunk / page_bytes;
         if (wp > n_pages) wp = n_pages;
         if (wp > slot_pages) slot_pages = wp;
     }

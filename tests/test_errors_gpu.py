@@ -66,6 +66,11 @@ def test_ecb_accepts_null_ivs(env):
 
 def test_enokey_and_key_errors(env):
     kg, torch, buf, x, out, iv, n, pb = env
+    # a fresh key table (other test files may have set id 200 in this process)
+    torch.cuda.synchronize()
+    assert kg.raw_lib().kg_shutdown() == kg.OK
+    kg.init(0)
+    kg.set_key(0, synth.make_key(16))
     assert rc(kg, 0, 0, x, out, n, pb, iv, 200) == kg.ENOKEY
     lib = kg.raw_lib()
     assert lib.kg_set_key(0, b"\0" * 20, 20) == kg.EINVAL
@@ -156,7 +161,7 @@ def test_enomem_staging_then_recovers():
     try:
         kg.wait(kg.submit_pages(1, 0, hx, hout, n, pb, hiv, 0))
     finally:
-        kg.set_pipeline(0, 4)
+        kg.set_pipeline(0, kg.DEFAULT_STAGING_SLOTS)
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
     from gpu_util import oracle_pages
     assert np.array_equal(hout.numpy(), oracle_pages(1, 0, key, data, n, pb, ivs))

@@ -156,5 +156,5 @@ def test_keyed_host_batches(direction, mode, path):
         kg.wait(kg.submit_pages_keyed(direction, mode, y, y, n, pb, hiv, did, 16))
         assert first_mismatch(y.numpy(), exp) is None
     finally:
-        kg.set_pipeline(0, 4)
+        kg.set_pipeline(0, kg.DEFAULT_STAGING_SLOTS)
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)

@@ -101,7 +101,7 @@ def test_small_staging_chunks_many_slots():
         try:
             got = gpu_pages(1, 0, key, data, n, pb, ivs, where="pinned")
         finally:
-            kg.set_pipeline(0, 4)
+            kg.set_pipeline(0, kg.DEFAULT_STAGING_SLOTS)
             kg.set_host_path(kg.HOST_AUTO, 32 << 20)
         assert first_mismatch(got, exp) is None, (chunk, slots)
 
@@ -185,7 +185,7 @@ def test_staged_batches_back_to_back():
             exp = oracle_pages(d, 0, key, data, n, pb, ivs)
             assert first_mismatch(hout.numpy(), exp) is None
     finally:
-        kg.set_pipeline(0, 4)
+        kg.set_pipeline(0, kg.DEFAULT_STAGING_SLOTS)
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
 
 
@@ -198,7 +198,7 @@ def test_staged_auto_chunks_warm_and_cold():
     from gpu_util import kg_ready
     kg, torch = kg_ready()
     kg.set_host_path(kg.HOST_STAGED)
-    kg.set_pipeline(0, 4)
+    kg.set_pipeline(0, kg.DEFAULT_STAGING_SLOTS)
     try:
         n, pb = 9000, 4096
         key = synth.make_key(32, seed=811)
@@ -333,7 +333,7 @@ def test_staged_device_input_one_batch_texture(direction, mode):
     try:
         kg.wait(kg.submit_pages(direction, mode, x, out, n, pb, iv, 0))
     finally:
-        kg.set_pipeline(0, 4)
+        kg.set_pipeline(0, kg.DEFAULT_STAGING_SLOTS)
         kg.set_host_path(kg.HOST_AUTO, 32 << 20)
     torch.cuda.synchronize()
     assert first_mismatch(out.numpy(), exp) is None
