@@ -46,6 +46,23 @@ for n, pb in [(3, 4096), (5, 48), (40, 512)]:
             x = data.clone()
             kg.wait(kg.submit_pages_keyed(d, mode, x, x, n, pb, ivs if mode == 0 else None, ids, 16))
             assert torch.equal(x, out)
+# staged batches back to back (warm schedule: no ramps, the slot rotation
+# continuing across batches), small chunks so every batch spans several slots
+kg.set_host_path(kg.HOST_STAGED)
+kg.set_pipeline(4 * 4096, 3)
+n, pb = 37, 4096
+hdata = torch.from_numpy(synth.make_pages(n, pb)).pin_memory()
+hivs = torch.from_numpy(synth.make_ivs(n)).pin_memory()
+streams = [torch.cuda.Stream() for _ in range(3)]
+outs = [torch.empty_like(hdata).pin_memory() for _ in range(4)]
+ts = [kg.submit_pages(b % 2, 0, hdata, outs[b], n, pb, hivs, 16, streams[b % 3]) for b in range(4)]
+for t in ts:
+    kg.wait(t)
+ref = torch.empty_like(hdata).pin_memory()
+kg.set_pipeline(0, kg.DEFAULT_STAGING_SLOTS)
+kg.set_host_path(kg.HOST_AUTO)
+kg.wait(kg.submit_pages(0, 0, hdata, ref, n, pb, hivs, 16))
+assert torch.equal(outs[0], ref) and torch.equal(outs[2], ref)
 kg.nsk_start(2, kg.NSK_DIRECT | kg.NSK_NOCAL, 2000)
 n, pb = 4, 4096
 data = torch.from_numpy(synth.make_pages(n, pb)).cuda()
