@@ -41,8 +41,8 @@
  * GPU (or managed memory) or page-locked ("pinned") host memory registered
  * with CUDA.  Pageable host memory -> KG_EINVAL.  Mixed kinds are allowed.
  * Device batches run on `stream`; batches touching host memory are staged
- * through the library's device staging ring (4 slots by default, after
- * PAPER.md:437-440's three buffers plus one) on internal copy/compute streams overlapped with each
+ * through the library's device staging ring (6 slots by default: PAPER.md:437-440's
+ * three buffers, plus room for the lagged D2H and back-to-back batches, profiles/r2_e2e) on internal copy/compute streams overlapped with each
  * other, joined back onto `stream`.
  */
 #ifndef KG_H

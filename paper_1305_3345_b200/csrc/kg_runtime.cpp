@@ -12,8 +12,8 @@
 //    concurrently with another service running on the GPU" and "on the GPU,
 //    we use three buffers ... one is used by the active service, a second
 //    may receive input ... a third may be copying the output" -> host-memory
-//    batches stream through a ring of device staging slots (default 4: the
-//    paper's three plus one for the lagged D2H) on an H2D stream, a compute
+//    batches stream through a ring of device staging slots (default 6: the
+//    paper's three, plus the lagged D2H and batches back to back, profiles/r2_e2e) on an H2D stream, a compute
 //    stream and a D2H stream ordered by events.
 //  * There is no user-space helper process and no kernel module: one address
 //    space, so the copy engines DMA straight from/to the caller's pinned
