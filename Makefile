@@ -80,7 +80,16 @@ build/soak_tsan: tools/soak_tsan.cpp $(CSRC)/kg_runtime.cpp $(CSRC)/kg_tables.cp
 	$(NVCC) $(ARCH) -o $@ tools/soak_tsan.cpp build/kg_runtime_tsan.o build/kg_tables_tsan.o build/kg_kernels.o \
 	  -Iinclude -Xcompiler -fsanitize=thread -ltsan -lpthread
 
+# bounds-checked library (KG_BOUNDS_CHECK: every global page/IV/key-id access checked, trap on a
+# violation; stands in for compute-sanitizer memcheck): KG_LIBKGPU=build/bounds/libkgpu_bounds.so
+bounds: build/bounds/libkgpu_bounds.so
+
+build/bounds/libkgpu_bounds.so: $(CSRC)/kg_kernels.cu $(CSRC)/kg_tables.cpp $(CSRC)/kg_runtime.cpp $(CSRC)/kg_internal.h $(wildcard $(CSRC)/*.cuh) include/kg.h
+	mkdir -p build/bounds
+	$(NVCC) $(NVFLAGS) -DKG_BOUNDS_CHECK -c $(CSRC)/kg_kernels.cu -o build/bounds/kg_kernels.o 2> build/bounds/kg_kernels.ptxas.txt || (cat build/bounds/kg_kernels.ptxas.txt; false)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ build/bounds/kg_kernels.o build/kg_tables.o build/kg_runtime.o -Xcompiler -fvisibility=hidden
+
 clean:
 	rm -rf build $(LIB) oracle/libkgo.so
 
-.PHONY: all clean tools
+.PHONY: all clean tools bounds

@@ -80,6 +80,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ uint32_t rotl32(uint32_t v, int s) { return __funnelshift_l(v, v, s); }
 
+// KG_BOUNDS_CHECK (diagnostics build, `make bounds` -> build/exp/libkgpu_bounds.so;
+// it stands in for compute-sanitizer memcheck, which this pool does not run):
+// every global page, IV and key-id access is checked against its batch's
+// extent and a violation traps (KG_ECUDA at kg_wait).  The product build
+// compiles the checks away.
+#ifdef KG_BOUNDS_CHECK
+#define KG_CHK(c)             \
+    do {                      \
+        if (!(c)) __trap();   \
+    } while (0)
+#else
+#define KG_CHK(c) \
+    do {          \
+    } while (0)
+#endif
+
 // Replicate the 256-entry base tables into the lane-private layout.  Warp w
 // owns entries [w*per, (w+1)*per): its lanes fetch them with ONE coalesced
 // load per table (all loads in flight at once), then the warp writes the 32
@@ -309,6 +325,7 @@ struct Job {
 // two texel fetches through the texture pipe.
 template <bool TEX>
 __device__ __forceinline__ void ld_pair(const Job &a, uint64_t q, uint4 &x0, uint4 &x1) {
+    KG_CHK(2 * q + 1 < a.n_pages * a.m);
     if (TEX) {
         const int i = (int)(a.tex_off + 2 * (int64_t)q);
         x0 = tex1Dfetch<uint4>((cudaTextureObject_t)a.tex, i);
@@ -348,7 +365,10 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
     if (CBC && DEC) {
         // Snapshot the predecessor of this warp's first block before anyone
         // in the CTA stores (in-place safety).
-        if (w0 < w1 && (w0 % m) != 0) carry = a.in[w0 - 1];
+        if (w0 < w1 && (w0 % m) != 0) {
+            KG_CHK(w0 - 1 < a.n_pages * m);
+            carry = a.in[w0 - 1];
+        }
     }
     // Software pipeline: the next unit's ciphertext is in flight while the
     // current unit's rounds run (hides the HBM latency behind the lookups).
@@ -359,6 +379,7 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
         const uint64_t g = u + lane;
         const bool act = g < w1;
         const uint4 c = c_next;
+        KG_CHK(g + 32 >= w1 || g + 32 < a.n_pages * m);
         c_next = (g + 32 < w1) ? ld_stream(a.in + g + 32) : make_uint4(0, 0, 0, 0);
         uint4 prev = make_uint4(0, 0, 0, 0);
         if (CBC && DEC) {
@@ -367,11 +388,13 @@ __device__ __forceinline__ void blockpar_body(const Job &a, const Cipher &cph, u
             const uint4 r = shfl4(c, (lane + 31) & 31);
             prev = (lane == 0) ? carry : r;
             carry = r;
+            KG_CHK(!(act && j == 0) || page < a.n_pages);
             if (act && j == 0) prev = a.ivs[page];
         }
         const auto kl = cph.lane(page);
         uint4 o = cph.rounds(kl, cph.first(kl, c));
         if (CBC && DEC) o = xor4(o, prev);
+        KG_CHK(!act || g < a.n_pages * m);
         if (act) st_stream(a.out + g, o);
         // advance (page, j) by 32 blocks
         j += 32;
@@ -423,6 +446,7 @@ __device__ __forceinline__ void group_stream(const Job &a, const Cipher &cph, ui
             const uint4 r = shfl4(x[G - 1], (lane + 31) & 31);
             prev = (lane == 0) ? carry : r;
             carry = r;
+            KG_CHK(!(act && jg == 0) || page < a.n_pages);
             if (act && jg == 0) prev = a.ivs[page];
         }
         const auto kl = cph.lane(page);
@@ -436,7 +460,10 @@ __device__ __forceinline__ void group_stream(const Job &a, const Cipher &cph, ui
         }
         if (act) {
 #pragma unroll
-            for (int h = 0; h < G / 2; ++h) st256<false>(a.out + G * q + 2 * h, o[2 * h], o[2 * h + 1]);
+            for (int h = 0; h < G / 2; ++h) {
+                KG_CHK(G * q + 2 * h + 1 < a.n_pages * a.m);
+                st256<false>(a.out + G * q + 2 * h, o[2 * h], o[2 * h + 1]);
+            }
         }
         jg += 32;
         if (jg >= mg) {
@@ -485,7 +512,10 @@ __device__ __forceinline__ void blockgroup_body(const Job &a, const Cipher &cph,
 
     uint4 carry = make_uint4(0, 0, 0, 0);
     if (CBC && DEC) {
-        if (w0 < w1 && (w0 % mg) != 0) carry = a.in[G * w0 - 1];
+        if (w0 < w1 && (w0 % mg) != 0) {
+            KG_CHK(G * w0 - 1 < a.n_pages * a.m);
+            carry = a.in[G * w0 - 1];
+        }
     }
     uint4 nx[G];
 #pragma unroll
@@ -506,6 +536,7 @@ __device__ __forceinline__ void blockgroup_body(const Job &a, const Cipher &cph,
         const uint32_t jl = (uint32_t)(q0 + lane - pg * mg);
         if (q0 + lane < c1) ld_group<G, TEX>(a, q0 + lane, nx);
         uint4 cr = make_uint4(0, 0, 0, 0);
+        KG_CHK(!(CBC && DEC && q0 % mg != 0) || G * q0 - 1 < a.n_pages * a.m);
         if (CBC && DEC && q0 % mg != 0) cr = a.in[G * q0 - 1];  // out of place only (in place: q0 is a page start)
         const uint64_t q1 = q0 + unit < c1 ? q0 + unit : c1;  // the last unit may be partial
         group_stream<G, DEC, CBC, TEX>(a, cph, q0, q1, mg, cr, pg, jl, nx);
@@ -531,6 +562,7 @@ __device__ __forceinline__ void cbc_enc_body(const Job &a, const Cipher &cph, ui
     for (uint64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const uint4 *src = a.in + p * m;
         uint4 *dst = a.out + p * m;
+        KG_CHK(p < a.n_pages);  // the page's blocks [p*m, p*m + m) and its IV
         uint4 prev = a.ivs[p];  // C_{p,-1} := IV_p
         const auto kl = cph.lane(p);
         if (WIDE) {
@@ -862,6 +894,7 @@ struct RegKeyPolicy {
         __device__ __forceinline__ uint4 operator()(int r) const { return l.k[r]; }
     };
     __device__ __forceinline__ L lane(uint64_t page) const {
+        KG_CHK(page < n_pages);
         uint32_t id = __ldg(ids + page);
         if (id >= (uint32_t)kMaxKeys || nr[id] != NR) {
             atomicOr(status, 1u);

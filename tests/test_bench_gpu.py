@@ -65,3 +65,17 @@ def test_bench_one_gpu_line_contract():
     c1 = d["c1"]
     assert c1["round_trip_equal"] and c1["sp800_38a_f21_encrypt_ok"] and c1["sp800_38a_f22_decrypt_ok"]
     assert 0 < c1["decrypt_us_p10_p50_p90"][1] < 1e4
+
+
+def test_bench_two_ranks_c5_strong_scaling():
+    """C5 (BASELINE.json:11, the config of the 1/2/4/8 scaling metric) under the
+    driver's --gpus N form: the 64 GiB job split into two contiguous page
+    ranges, each rank checking EVERY byte of its range against the M-page
+    pattern at its own offset (synth.shard; bench.plan)."""
+    d = _run(["--gpus", "2", "--workload", "c5", "--extra", "none", "--steps", "2", "--warmup", "3", "--no-e2e"],
+             {"KG_BENCH_SHARE_GPU": "1"}, timeout=1200)
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["comm"]["world"] == 2
+    assert d["config"]["n_pages_per_gpu"] == 16777216 // 2
+    assert d["check"]["pages"] == 16777216 and d["check"]["mismatched_pages"] == 0
+    assert d["gpu_launches"] >= 2 * 2
+    assert 0 < d["roofline"]["frac"] < 1.05
