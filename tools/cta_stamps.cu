@@ -153,6 +153,26 @@ int main(int argc, char **argv) {
         }
         printf("]}\n");
     }
+    // KG_STAMPS_ALL=1: per-CTA rows of every recorded launch, times in us from the
+    // first recorded start: [launch, cta, smid, start, wait release, first warp done, last warp done]
+    if (getenv("KG_STAMPS_ALL")) {
+        printf("{\"per_cta_all\": [");
+        bool first = true;
+        for (size_t k = 0; k < order.size(); k++) {
+            auto &L = h[order[k]];
+            for (int c = 0; c < 148; c++) {
+                unsigned long long dmin = ~0ull, dmax = 0;
+                for (int w = 0; w < warps; w++) {
+                    dmin = std::min(dmin, L[c][3 + w]);
+                    dmax = std::max(dmax, L[c][3 + w]);
+                }
+                printf("%s[%zu, %d, %llu, %.3f, %.3f, %.3f, %.3f]", first ? "" : ", ", k, c, L[c][kg::kStampW - 1],
+                       (L[c][0] - t0) * 1e-3, (L[c][2] - t0) * 1e-3, (dmin - t0) * 1e-3, (dmax - t0) * 1e-3);
+                first = false;
+            }
+        }
+        printf("]}\n");
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e));
     return 0;
