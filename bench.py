@@ -935,10 +935,79 @@ def run_ours(args):
                            "sample": f"{n1} seeded 4 KiB pages ({n1 * PB / 2**20:.1f} MiB), 1 thread, {d1:.1f} s"}}
         line["context"] = {"openssl_aesni_1core": openssl_rate(key_bytes, direction)}
     print(json.dumps(line), flush=True)
+    if args.csv:
+        write_csv(args.csv, line)
     if ctx.dist:
         ctx.dist.barrier()
         ctx.dist.destroy_process_group()
     return 0
+
+
+CSV_COLUMNS = ("config", "dir", "key_bits", "residency", "gpus", "n_pages", "page_bytes", "latency_us_p50", "gbps",
+               "roofline_gbps", "pct_roofline", "sm_mhz_median", "host_cores")
+
+
+def csv_rows(line):
+    """The line's measurements as rows with SURVEY.md §5's columns (SPEC.md:470's
+    experiment CSV, extended): one row per config and residency (hbm = the
+    device-timed value; pinned = its e2e), one per C4 sweep point and path.
+    latency_us_p50 is the per-step time for the configs (K back-to-back steps)
+    and the caller-observed p50 for the sweep; roofline_gbps is the lookup bound
+    (pinned rows: the duplex host link measured in the same run)."""
+    rows = []
+    mhz = (line.get("clocks") or {}).get("sm_mhz")
+    cores = (line.get("cpu_baseline") or {}).get("cores", "")
+    heads = [(line["config"]["name"], line)] + sorted((line.get("configs") or {}).items())
+    for name, c in heads:
+        cfg = c.get("config", c)
+        dirn, kbits = cfg.get("dir", c.get("dir")), cfg.get("key_bits", c.get("key_bits"))
+        n = cfg.get("n_pages_per_gpu", c.get("n_pages_per_gpu"))
+        roof = c["roofline"]
+        rows.append({"config": name, "dir": dirn, "key_bits": kbits, "residency": "hbm", "gpus": line["n_gpus"],
+                     "n_pages": n, "page_bytes": PB, "latency_us_p50": round(1e3 * c["ms_per_step"], 3),
+                     "gbps": round(c["value"], 3), "roofline_gbps": round(roof["peak"], 3),
+                     "pct_roofline": round(100 * roof["frac"], 2),
+                     "sm_mhz_median": (c.get("clocks") or {}).get("sm_mhz", mhz), "host_cores": cores})
+        e = c.get("e2e")
+        if e:
+            link = e.get("link_duplex_aggregate_gbs_per_direction")
+            rows.append({"config": name, "dir": dirn, "key_bits": kbits, "residency": "pinned", "gpus": line["n_gpus"],
+                         "n_pages": n, "page_bytes": PB,
+                         "latency_us_p50": round(1e3 * e["step_ms_min_median_max"][1], 3)
+                         if e.get("step_ms_min_median_max") else "",
+                         "gbps": round(e["value"], 3), "roofline_gbps": round(link, 3) if link else "",
+                         "pct_roofline": round(100 * e["value"] / link, 2) if link else "",
+                         "sm_mhz_median": (c.get("clocks") or {}).get("sm_mhz", mhz), "host_cores": cores})
+    sw = line.get("c4_sweep")
+    if sw:
+        peak = compute_peak_gbs(16, float((line.get("clocks") or {}).get("sm_max_mhz") or 1965.0))
+        link = (line.get("e2e") or {}).get("link_duplex_aggregate_gbs_per_direction")
+        threads = {"oracle_1thread": 1, "oracle_threads": sw.get("oracle_threads", cores), "openssl_1core": 1}
+        paths = (("hbm_us", "hbm"), ("pinned_us", "pinned"), ("nsk_hbm_us", "hbm_nsk"), ("auto_hbm_us", "hbm_auto"),
+                 ("oracle_1t_us", "oracle_1thread"), ("oracle_T_us", "oracle_threads"),
+                 ("openssl_1core_us", "openssl_1core"))
+        for r in sw["rows"]:
+            for key, res in paths:
+                if key not in r:
+                    continue
+                gbs = r["pages"] * PB / (r[key] * 1e-6) / 1e9
+                gpu = res.startswith(("hbm", "pinned"))
+                bound = (link if res == "pinned" else peak) if gpu else None
+                rows.append({"config": "c4", "dir": "decrypt", "key_bits": 128, "residency": res, "gpus": 1,
+                             "n_pages": r["pages"], "page_bytes": PB, "latency_us_p50": r[key], "gbps": round(gbs, 3),
+                             "roofline_gbps": round(bound, 3) if bound else "",
+                             "pct_roofline": round(100 * gbs / bound, 2) if bound else "",
+                             "sm_mhz_median": mhz if gpu else "", "host_cores": "" if gpu else threads[res]})
+    return rows
+
+
+def write_csv(path, line):
+    import csv
+    with open(path, "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=CSV_COLUMNS)
+        w.writeheader()
+        for r in csv_rows(line):
+            w.writerow(r)
 
 
 def free_port():
@@ -984,6 +1053,8 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--queue-ahead-steps", type=int, default=3,
                     help="untimed steps enqueued after the barrier, right before the start event (0: none)")
+    ap.add_argument("--csv", default="",
+                    help="also write the line's measurements as CSV rows (SURVEY.md §5 columns) to this path")
     ap.add_argument("--ref-step-seconds", type=float, default=0.0,
                     help="reference arm: oracle seconds per step (default: sized so the run takes ~2.5 min)")
     args = ap.parse_args(argv)

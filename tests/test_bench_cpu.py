@@ -50,3 +50,29 @@ def test_load_peaks_tolerates_key_names(tmp_path, monkeypatch):
     assert bench.load_peaks()["_fallback"] is True
     (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps({"something": 1}))
     assert bench.load_peaks()["_fallback"] is True
+
+
+def test_csv_rows_from_a_line():
+    """--csv: the line's numbers as SURVEY.md §5 rows (one per config x residency,
+    one per sweep point x path), computed from the JSON line alone."""
+    sys.path.insert(0, ROOT)
+    import bench
+    roof = {"peak": 930.624, "frac": 0.9}
+    line = {"n_gpus": 1, "config": {"name": "c2", "dir": "decrypt", "key_bits": 128, "n_pages_per_gpu": 65536},
+            "value": 837.5616, "ms_per_step": 0.3205, "roofline": roof, "clocks": {"sm_mhz": 1965, "sm_max_mhz": 1965},
+            "e2e": {"value": 48.0, "step_ms_min_median_max": [5.4, 5.5, 5.6],
+                    "link_duplex_aggregate_gbs_per_direction": 50.0},
+            "cpu_baseline": {"cores": 16},
+            "configs": {"c3": {"dir": "encrypt", "key_bits": 256, "n_pages_per_gpu": 262144, "value": 600.0,
+                               "ms_per_step": 1.79, "roofline": {"peak": 664.73, "frac": 0.9026}, "e2e": None}},
+            "c4_sweep": {"oracle_threads": 16,
+                         "rows": [{"pages": 1, "hbm_us": 16.384, "pinned_us": 20.0, "oracle_T_us": 2000.0}]}}
+    rows = bench.csv_rows(line)
+    assert [tuple(r[k] for k in ("config", "residency")) for r in rows] == [
+        ("c2", "hbm"), ("c2", "pinned"), ("c3", "hbm"), ("c4", "hbm"), ("c4", "pinned"), ("c4", "oracle_threads")]
+    assert all(set(r) == set(bench.CSV_COLUMNS) for r in rows)
+    assert rows[0]["gbps"] == 837.562 and rows[0]["pct_roofline"] == 90.0 and rows[0]["latency_us_p50"] == 320.5
+    assert rows[1]["pct_roofline"] == 96.0 and rows[1]["roofline_gbps"] == 50.0
+    assert rows[2]["key_bits"] == 256 and rows[2]["n_pages"] == 262144
+    assert rows[3]["gbps"] == 0.25 and rows[4]["roofline_gbps"] == 50.0        # 4096 B / 16.384 us; pinned vs the link
+    assert rows[5]["host_cores"] == 16 and rows[5]["roofline_gbps"] == ""

@@ -46,9 +46,16 @@ def test_bench_two_ranks_self_launched():
     assert "cpu_baseline" not in d                       # rank 0 at N=1 only
 
 
-def test_bench_one_gpu_line_contract():
+def test_bench_one_gpu_line_contract(tmp_path):
+    csv_path = tmp_path / "bench.csv"
     d = _run(["--steps", "5", "--warmup", "3", "--extra", "c3,c4_1gib", "--sweep-kmax", "6",
-              "--sweep-nsk-pages", "4", "--cpu-seconds", "2"])
+              "--sweep-nsk-pages", "4", "--cpu-seconds", "2", "--csv", str(csv_path)])
+    import csv
+    with open(csv_path) as f:
+        rows = list(csv.DictReader(f))
+    assert {(r["config"], r["residency"]) for r in rows} >= {("c2", "hbm"), ("c2", "pinned"), ("c3", "hbm"),
+                                                             ("c4_1gib", "pinned"), ("c4", "hbm"), ("c4", "pinned")}
+    assert abs(float(rows[0]["gbps"]) - d["value"]) < 1e-2
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline"):
         assert k in d, k
